@@ -1,0 +1,137 @@
+"""Independent test helpers: golden-file readers, brute-force GF(2) and MAP.
+
+Nothing here calls the oracle or the CUDA library; these are the "something
+other than itself" that the oracle's pins compare against.
+"""
+from __future__ import annotations
+
+import math
+import os
+
+import numpy as np
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def golden_lines(name: str) -> list[list[str]]:
+    out = []
+    with open(os.path.join(GOLDEN, name)) as f:
+        for line in f:
+            line = line.strip()
+            if line and not line.startswith("#"):
+                out.append(line.split())
+    return out
+
+
+def golden_matrix(name: str) -> np.ndarray:
+    return np.array([[int(x) for x in row] for row in golden_lines(name)], dtype=np.uint8)
+
+
+def hamming74_H() -> np.ndarray:
+    """Textbook Hamming(7,4): column j (1-based) is the binary expansion of j."""
+    return np.array([[(j >> b) & 1 for j in range(1, 8)] for b in range(3)], dtype=np.uint8)
+
+
+def gf2_rank(H: np.ndarray) -> int:
+    """GF(2) rank by left-to-right elimination on Python-int rows (independent
+    of the oracle's right-to-left bit-packed Gauss-Jordan)."""
+    rows = [int("".join(str(int(b)) for b in r[::-1]) or "0", 2) for r in np.asarray(H)]
+    rank = 0
+    ncols = H.shape[1]
+    for col in range(ncols):
+        bit = 1 << col
+        piv = None
+        for i in range(rank, len(rows)):
+            if rows[i] & bit:
+                piv = i
+                break
+        if piv is None:
+            continue
+        rows[rank], rows[piv] = rows[piv], rows[rank]
+        for i in range(len(rows)):
+            if i != rank and rows[i] & bit:
+                rows[i] ^= rows[rank]
+        rank += 1
+    return rank
+
+
+def codewords(H: np.ndarray) -> np.ndarray:
+    """All x in GF(2)^n with H x = 0, by enumeration (n <= 20)."""
+    H = np.asarray(H, dtype=np.int64)
+    m, n = H.shape
+    assert n <= 20
+    xs = ((np.arange(1 << n)[:, None] >> np.arange(n)[None, :]) & 1).astype(np.int64)
+    s = (xs @ H.T) % 2
+    return xs[np.all(s == 0, axis=1)].astype(np.uint8)
+
+
+def map_llr(H: np.ndarray, R: np.ndarray) -> np.ndarray:
+    """Exact bitwise-MAP posterior LLRs ln(P(x_v=1|y)/P(x_v=0|y)) for LLR inputs
+    R = ln(p1/p0) of independent bits, uniform prior over the code:
+    P(x) ~ prod_u exp(x_u R_u).  Brute force over all codewords."""
+    cw = codewords(H).astype(np.float64)
+    R = np.asarray(R, dtype=np.float64)
+    score = cw @ R
+    out = np.zeros(H.shape[1])
+    for v in range(H.shape[1]):
+        s1 = score[cw[:, v] == 1]
+        s0 = score[cw[:, v] == 0]
+        out[v] = _lse(s1) - _lse(s0)
+    return out
+
+
+def _lse(a: np.ndarray) -> float:
+    if a.size == 0:
+        return -math.inf
+    mx = a.max()
+    return float(mx + np.log(np.exp(a - mx).sum()))
+
+
+def ml_decode(H: np.ndarray, R: np.ndarray) -> np.ndarray:
+    """Block ML codeword: argmax_x sum_u x_u R_u over the code."""
+    cw = codewords(H)
+    return cw[np.argmax(cw.astype(np.float64) @ np.asarray(R, dtype=np.float64))]
+
+
+def random_tree_H(rng: np.random.Generator, n_max: int = 16) -> np.ndarray:
+    """A random cycle-free Tanner graph whose checks all have degree >= 2:
+    grow from one variable; each new check attaches to one existing variable
+    and 1..3 new ones."""
+    nv = 1
+    checks = []
+    while True:
+        add = int(rng.integers(1, 4))
+        if nv + add > n_max:
+            break
+        anchor = int(rng.integers(0, nv))
+        checks.append([anchor] + list(range(nv, nv + add)))
+        nv += add
+    H = np.zeros((len(checks), nv), dtype=np.uint8)
+    for c, vs in enumerate(checks):
+        H[c, vs] = 1
+    # random relabelling of variables and checks keeps it a tree
+    H = H[rng.permutation(H.shape[0])][:, rng.permutation(nv)]
+    return H
+
+
+def is_tree(H: np.ndarray) -> bool:
+    """Connected and |E| = |V| + |C| - 1."""
+    m, n = H.shape
+    edges = int(H.sum())
+    if edges != m + n - 1:
+        return False
+    seen = {("v", 0)}
+    stack = [("v", 0)]
+    while stack:
+        kind, i = stack.pop()
+        nbrs = [("c", c) for c in np.nonzero(H[:, i])[0]] if kind == "v" else \
+               [("v", v) for v in np.nonzero(H[i])[0]]
+        for nb in nbrs:
+            if nb not in seen:
+                seen.add(nb)
+                stack.append(nb)
+    return len(seen) == m + n
+
+
+def q_function(x: float) -> float:
+    return 0.5 * math.erfc(x / math.sqrt(2.0))
