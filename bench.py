@@ -1,0 +1,383 @@
+#!/usr/bin/env python3
+"""Benchmark of the hot path: batched LDPC encode + Sum-Product decode + error
+count (+ NCCL all-reduce of the counters when N > 1) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C4] [--frames F]
+
+One step = one pass of every §8(a) row over one batch of synthetic frames
+resident in HBM: ldpc_encode (e1) -> ldpc_decode (a1-a8) -> ldpc_count_errors
+(a9) -> all_reduce(int64[6]) (a9, N > 1).  Default workload: BASELINE.json
+configs[3] (C4: n = 16200 (3,6), 200,000 frames, 50 fixed iterations,
+Eb/N0 1.5 dB, with the bit-packed encode of all frames) -- the largest config
+that fits one GPU (C5's 1,000,000 frames of n = 64800 need 259 GB of LLRs).
+Frames shard across ranks by Eq. 9 (weak scaling: every rank decodes its own
+batch; frame indices are global so results do not depend on N).
+
+Rank 0 prints one JSON line.  `--impl reference` times the CPU oracle on the
+host cores (the reference arm for this paper-only tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import ldpc_workloads as W  # noqa: E402
+
+# SFU roofline: 4 MUFU ops per edge-update (2 phi per
+# edge per iteration, ex2 + lg2 each), 16 MUFU/clk/SM, 148 SMs.
+MUFU_PER_CLK_PER_SM = 16
+MUFU_PER_EDGE_UPDATE = 4
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C4", choices=sorted(W.ALL))
+    ap.add_argument("--frames", type=int, default=0, help="override frames per GPU per step")
+    ap.add_argument("--e2e-frames", type=int, default=65536)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--variant", type=int, default=0)
+    return ap.parse_args()
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[2 + i]
+                          and "Not" not in s[2 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------- reference arm
+def cpu_oracle_run(wl, frames_per_thread: int, threads: int):
+    """Time the oracle (as it stands) decoding a bounded sample of the workload
+    on `threads` host threads.  Returns (seconds, frames, k)."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as O
+    code = O.make_H(wl.n, wl.wc, wl.wr, W.CODE_SEED)
+    code.make_G() if wl.n <= 20000 else None
+    k = code.k if code.k is not None else wl.n - code.m + (wl.wc - 1)
+    F = frames_per_thread * threads
+    if code.k is not None:
+        info = O.gen_info(wl.frame_seeds[0], 0, F, code.k)
+        c = O.encode(code, info)
+    else:
+        c = np.zeros((F, wl.n), np.uint8)
+    R = O.channel(wl.frame_seeds[0], 0, c, wl.sigma())
+    chunks = np.array_split(np.arange(F), threads)
+
+    def run(idx):
+        if len(idx):
+            O.spa_decode(code, R[idx], wl.max_iter, wl.early_term)
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(run, chunks))
+    return time.perf_counter() - t0, F, k
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    wl = W.ALL[args.config]
+    threads = max(1, min(os.cpu_count() or 1, 128))
+    per_thread = 1
+    # warm-up / timed steps, each a bounded sample (one frame per host thread)
+    for _ in range(args.warmup):
+        cpu_oracle_run(wl, per_thread, threads)
+    times = []
+    for _ in range(args.steps):
+        dt, F, k = cpu_oracle_run(wl, per_thread, threads)
+        times.append(dt)
+    T = sum(times)
+    value = args.steps * F * k / T / 1e9
+    sample = f"{F} frames of {wl.name} per step ({per_thread} per host thread), {wl.max_iter} iterations"
+    line = {
+        "impl": "reference", "metric": "decoded info Gbit/s", "value": value, "unit": "Gbit/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "long double (x87 f80)",
+        "data": "synthetic (seeded Philox frames, BASELINE.json recipe)",
+        "config": workload_config(wl, F, args.gpus),
+        "cpu_baseline": {"value": value, "unit": "Gbit/s", "cores": threads, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(wl, frames, gpus):
+    return {"workload": f"{wl.name}: Gallager ({wl.wc},{wl.wr}) n={wl.n}, {wl.frames} frames in BASELINE.json, "
+                        f"{wl.max_iter} {'max (early term.)' if wl.early_term else 'fixed'} SPA iterations, "
+                        f"BPSK/AWGN Eb/N0={wl.ebn0_db[0]} dB, fp32 LLRs",
+            "n": wl.n, "wc": wl.wc, "wr": wl.wr, "frames_per_gpu_per_step": frames, "iterations": wl.max_iter,
+            "early_term": wl.early_term, "ebn0_db": wl.ebn0_db[0], "sigma": wl.sigma(), "code_seed": W.CODE_SEED,
+            "frame_seed": wl.frame_seeds[0], "parallelism": f"dp{gpus} (frames sharded by Eq. 9, weak scaling)",
+            "l2_policy": "inputs larger than L2 (LLR batch >> 126 MB), no flush needed"}
+
+
+# --------------------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2201_04265_b200 as L
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    wl = W.ALL[args.config]
+    frames = args.frames or (wl.frames if wl.frames * wl.n * 4 < 40e9 else 16384)
+    props = torch.cuda.get_device_properties(dev)
+    sms = props.multi_processor_count
+
+    # ---- setup (untimed): code, device image, frames
+    t_setup = time.perf_counter()
+    code = L.ldpc_make_H(wl.n, wl.wc, wl.wr, W.CODE_SEED)
+    L.ldpc_make_G(code)
+    L.ldpc_code_bind_device(code, dev)
+    info = code.info
+    n, k = info.n, info.k
+    kw, nw = L.words(k), L.words(n)
+    frame0 = rank * frames       # global frame indices: rank r owns [r F, (r+1) F)
+    d_info = torch.empty((frames, kw), dtype=torch.int32, device=dev)
+    d_cw = torch.empty((frames, nw), dtype=torch.int32, device=dev)
+    d_llr = torch.empty((frames, n), dtype=torch.float32, device=dev)
+    d_bits = torch.empty((frames, nw), dtype=torch.int32, device=dev)
+    d_syn = torch.empty(frames, dtype=torch.uint8, device=dev)
+    d_it = torch.empty(frames, dtype=torch.int32, device=dev)
+    d_ctr = torch.zeros(6, dtype=torch.int64, device=dev)
+    wsb = L.ldpc_decode_workspace_bytes(code, frames, wl.max_iter, wl.early_term, args.variant)
+    d_ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev) if wsb else None
+    seed = wl.frame_seeds[0]
+    L.ldpc_gen_info(seed, frame0, frames, k, d_info)
+    L.ldpc_encode(code, d_info, d_cw, frames)
+    L.ldpc_channel(code, seed, frame0, frames, d_cw, wl.sigma(), d_llr)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+    stream = torch.cuda.current_stream()
+
+    def step():
+        L.ldpc_encode(code, d_info, d_cw, frames)
+        ev_d0.record(stream)
+        L.ldpc_decode(code, d_llr, frames, d_bits, d_syn, d_it, None, d_ws, wl.max_iter, wl.early_term,
+                      args.variant)
+        ev_d1.record(stream)
+        d_ctr.zero_()
+        L.ldpc_count_errors(code, d_info, d_bits, d_cw, d_syn, d_it, frames, d_ctr)
+        if world > 1:
+            dist.all_reduce(d_ctr)
+
+    ev_d0 = torch.cuda.Event(enable_timing=True)
+    ev_d1 = torch.cuda.Event(enable_timing=True)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    dec_ms = []
+    with ClockSampler(dev.index if world == 1 else local) as clk:
+        for i in range(args.steps):
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+            # decode kernel time of this step (events on the launching stream)
+            ends[i].synchronize()
+            dec_ms.append(ev_d0.elapsed_time(ev_d1))
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+    t = torch.tensor([total_ms, sum(dec_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, dec_total_ms = float(t[0]), float(t[1])
+    ctr = d_ctr.cpu().numpy()
+    iters_mean = float(ctr[4]) / max(float(ctr[5]), 1.0)
+
+    all_frames = frames * world * args.steps
+    value = all_frames * k / (total_ms / 1e3) / 1e9
+    edge_updates = float(ctr[4]) * wl.edges * (args.steps if world == 1 else args.steps)  # executed iterations
+    edge_updates_per_step_rank = float(ctr[4]) / world * wl.edges
+    dec_avg_s = dec_total_ms / args.steps / 1e3
+    achieved = edge_updates_per_step_rank / dec_avg_s / 1e9            # Gedge-updates/s, one GPU
+    clock_mhz = measured_peaks().get("sm_max_mhz", 1965.0)
+    peak = sms * MUFU_PER_CLK_PER_SM * clock_mhz * 1e6 / MUFU_PER_EDGE_UPDATE / 1e9
+    clocks = clk.summary()
+
+    # ---- end to end through the public API with host buffers (rank-local)
+    e2e = e2e_measure(L, code, wl, args, dev, frame0, k, n, kw, nw, world)
+
+    # ---- CPU baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = max(1, min(os.cpu_count() or 1, 128))
+        dt, F, kk = cpu_oracle_run(wl, 1, threads)
+        cpu = {"value": F * kk / dt / 1e9, "unit": "Gbit/s", "cores": threads, "kind": "oracle",
+               "sample": f"{F} frames of {wl.name} ({wl.max_iter} iterations), one per host thread, "
+                         f"{dt:.1f} s wall"}
+
+    if rank == 0:
+        line = {
+            "metric": "decoded info Gbit/s", "value": value, "unit": "Gbit/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded Philox info bits, BPSK/AWGN LLRs; BASELINE.json recipe)",
+            "config": workload_config(wl, frames, world),
+            "edge_updates_per_s": edge_updates_per_step_rank * world / (total_ms / args.steps / 1e3),
+            "decode_ms_per_step": dec_total_ms / args.steps,
+            "mean_iterations": iters_mean, "k": k,
+            "counters": {"info_bit_errors": int(ctr[0]), "cw_bit_errors": int(ctr[1]),
+                         "frame_errors": int(ctr[2]), "undetected": int(ctr[3]), "frames": int(ctr[5])},
+            "roofline": {"bound": "alu", "kernel": "spa_decode_kernel", "achieved": achieved, "peak": peak,
+                         "unit": "Gedge-updates/s", "frac": achieved / peak, "traffic": None,
+                         "peak_basis": f"SFU: {sms} SMs x 16 MUFU/clk x {clock_mhz:.0f} MHz / 4 MUFU per "
+                                       "edge-update (DESIGN.md)"},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks,
+            "gpu_launches": 3 * args.steps,
+            "setup_s": setup_s,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e_measure(L, code, wl, args, dev, frame0, k, n, kw, nw, world):
+    """Same metric through the public API with pinned host buffers: H2D of the
+    step's info bits and LLRs, encode, decode, count, D2H of the decoded bits
+    and the counters, all inside the timed region."""
+    import torch
+    F = min(args.e2e_frames, args.frames or wl.frames)
+    try:
+        h_info = torch.empty((F, kw), dtype=torch.int32, pin_memory=True)
+        h_llr = torch.empty((F, n), dtype=torch.float32, pin_memory=True)
+        h_bits = torch.empty((F, nw), dtype=torch.int32, pin_memory=True)
+        h_ctr = torch.empty(6, dtype=torch.int64, pin_memory=True)
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "unit": "Gbit/s", "error": f"pinned alloc failed: {e}"}
+    # fill the host inputs with the workload's frames (generated once, untimed)
+    d_info = torch.empty((F, kw), dtype=torch.int32, device=dev)
+    d_cw = torch.empty((F, nw), dtype=torch.int32, device=dev)
+    d_llr = torch.empty((F, n), dtype=torch.float32, device=dev)
+    seed = wl.frame_seeds[0]
+    L.ldpc_gen_info(seed, frame0, F, k, d_info)
+    L.ldpc_encode(code, d_info, d_cw, F)
+    L.ldpc_channel(code, seed, frame0, F, d_cw, wl.sigma(), d_llr)
+    h_info.copy_(d_info)
+    h_llr.copy_(d_llr)
+    d_bits = torch.empty((F, nw), dtype=torch.int32, device=dev)
+    d_syn = torch.empty(F, dtype=torch.uint8, device=dev)
+    d_it = torch.empty(F, dtype=torch.int32, device=dev)
+    d_ctr = torch.zeros(6, dtype=torch.int64, device=dev)
+    wsb = L.ldpc_decode_workspace_bytes(code, F, wl.max_iter, wl.early_term, args.variant)
+    d_ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev) if wsb else None
+
+    def step():
+        d_info.copy_(h_info, non_blocking=True)
+        d_llr.copy_(h_llr, non_blocking=True)
+        L.ldpc_encode(code, d_info, d_cw, F)
+        L.ldpc_decode(code, d_llr, F, d_bits, d_syn, d_it, None, d_ws, wl.max_iter, wl.early_term, args.variant)
+        d_ctr.zero_()
+        L.ldpc_count_errors(code, d_info, d_bits, d_cw, d_syn, d_it, F, d_ctr)
+        h_bits.copy_(d_bits, non_blocking=True)
+        h_ctr.copy_(d_ctr, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    steps = max(1, args.steps)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(steps):
+        step()
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e)
+    bi = F * kw * 4 + F * n * 4
+    bo = F * nw * 4 + 6 * 8
+    return {"value": world * steps * F * k / (ms / 1e3) / 1e9, "unit": "Gbit/s", "h2d_bytes_per_step": bi,
+            "d2h_bytes_per_step": bo, "frames_per_gpu_per_step": F,
+            "note": "pinned host buffers; copies serialised with compute on one stream"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

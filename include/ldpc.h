@@ -1,0 +1,194 @@
+/*
+ * ldpc.h -- C ABI of libldpc_b200.so: batched Sum-Product LDPC decoding on
+ * NVIDIA B200 (sm_100a), after arXiv 2201.04265 ("distributed LDPC encoding
+ * and Sum-Product decoding with MPI").  Citations: P:<line> = a line of the
+ * paper text, S:<line> = a line of the CPU-program spec;
+ * "reading Qn" = an interpretation listed in DESIGN.md.
+ *
+ * General contract
+ *  - Every call returns ldpc_status; nothing throws or aborts across the ABI.
+ *  - Bits are packed LSB-first into uint32 words.  A frame of b bits occupies
+ *    ceil(b/32) words; pad bits are written 0 and ignored on input.
+ *  - Every length-n vector is in H's column order (the variable-node order of
+ *    the Tanner graph).  The k information bits of a codeword sit at
+ *    positions perm[0..k) (ldpc_code_copy_perm), in message order.
+ *  - LLRs are L = ln(p(bit=1)/p(bit=0)), positive favours 1 (Eq. 4, P:121-125,
+ *    with the missing logarithm restored: reading Q1); z = 1 iff L >= 0
+ *    (Eq. 8).
+ *  - Device pointers (d_*) are caller-owned device memory (PyTorch allocates
+ *    everything; the library never allocates device memory).  Host pointers
+ *    are caller-owned host memory.  `stream` is a cudaStream_t passed as void*
+ *    (NULL = the legacy default stream).
+ *  - Device calls are asynchronous: argument errors and launch errors are
+ *    returned synchronously (LDPC_ERR_ARG / LDPC_ERR_CUDA); device faults
+ *    surface at the caller's next synchronisation of `stream`.
+ *  - An ldpc_code is immutable after ldpc_make_G + ldpc_code_bind_device, and
+ *    may then be used concurrently from several streams.
+ */
+#ifndef LDPC_B200_H
+#define LDPC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    LDPC_OK = 0,
+    LDPC_ERR_ARG = 1,            /* bad argument (NULL, out of range, bad size)          */
+    LDPC_ERR_NOT_DIVISIBLE = 2,  /* wr does not divide n (band construction)       */
+    LDPC_ERR_NO_INFO_BITS = 3,   /* rank(H) == n, so k == 0                       */
+    LDPC_ERR_DIM = 4,            /* dimension mismatch               */
+    LDPC_ERR_STATE = 5,          /* call out of order (e.g. encode before make_G / bind)  */
+    LDPC_ERR_UNSUPPORTED = 6,    /* e.g. a check degree > 32                               */
+    LDPC_ERR_CUDA = 7,           /* a CUDA runtime call failed                             */
+    LDPC_ERR_NOMEM = 8           /* host allocation failed                                 */
+} ldpc_status;
+
+typedef struct ldpc_code ldpc_code;   /* opaque; owns host memory only */
+
+typedef struct {
+    int32_t n;              /* code length (variable nodes)                        */
+    int32_t m;              /* parity checks (rows of H, check nodes)              */
+    int32_t k;              /* information bits = n - rank(H); -1 before make_G    */
+    int32_t rank;           /* GF(2) rank of H; -1 before make_G                   */
+    int32_t nnz;            /* Tanner-graph edges = ones of H                      */
+    int32_t max_row_deg;    /* max check degree                                    */
+    int32_t max_col_deg;    /* max variable degree                                 */
+    int32_t wc, wr;         /* Gallager column/row weight, 0 for an external H     */
+    int32_t gallager;       /* 1 if built by ldpc_make_H (band structure known)    */
+    double design_rate;     /* 1 - wc/wr, or 1 - m/n for an external H      */
+    size_t device_bytes;    /* bytes ldpc_code_bind_device needs                   */
+} ldpc_code_info;
+
+typedef struct {
+    int32_t max_iter;       /* >= 1: SPA iterations ("predefined number")   */
+    int32_t early_term;     /* 0: run exactly max_iter (paper); 1: stop after the  */
+                            /* first iteration t >= 1 whose z^t has zero syndrome  */
+                            /* (reading Q11 / c6)                                  */
+    int32_t variant;        /* 0 = auto; see ldpc_decode                           */
+    int32_t reserved;
+} ldpc_decode_opts;
+
+/* ---------------------------------------------------------------- codes */
+
+/* Regular (wc, wr) Gallager parity-check matrix (band
+ * construction S:52): wc bands of n/wr rows; band 0 row c has ones at columns
+ * [c*wr, (c+1)*wr); band b >= 1 is the column permutation pi_b of band 0
+ * drawn by Fisher-Yates (i = n-1..1, j = U(i+1), swap) from SplitMix64(seed),
+ * U by rejection (reading Q12).  Requires 1 <= wc < wr, n > 0.
+ * Errors: LDPC_ERR_NOT_DIVISIBLE if n % wr != 0; LDPC_ERR_ARG otherwise.
+ * *out receives a new code (free with ldpc_code_free). */
+ldpc_status ldpc_make_H(int32_t n, int32_t wc, int32_t wr, uint64_t seed, ldpc_code **out);
+
+/* An external parity-check matrix given as CSR (P:4: "Any Binary Parity Check
+ * matrix ... can be used"): row_ptr[m+1], col_idx[nnz] (host).  Duplicate
+ * entries in a row are rejected (LDPC_ERR_ARG); rows may be empty; check
+ * degrees must be <= 32 (LDPC_ERR_UNSUPPORTED). */
+ldpc_status ldpc_code_from_csr(int32_t m, int32_t n, const int32_t *row_ptr,
+                               const int32_t *col_idx, ldpc_code **out);
+
+/* Generator in standard form (Eq. 2-3): Gauss-Jordan
+ * elimination of H over GF(2), columns scanned right to left, pivot = lowest
+ * row index >= r (reading Q13).  Sets rank, k = n - rank, perm = [free
+ * columns ascending, pivot columns ascending] and P (k x (n-k)) with
+ * codeword = [m | m P] scattered by perm.  Host CPU, multi-threaded.
+ * Errors: LDPC_ERR_NO_INFO_BITS if k == 0. */
+ldpc_status ldpc_make_G(ldpc_code *code);
+
+ldpc_status ldpc_code_query(const ldpc_code *code, ldpc_code_info *info);
+
+/* Host copies for tests: dense H as m*n bytes (0/1, row-major); the column
+ * permutation (n int32); P packed column-major by parity bit:
+ * (n-k) * ceil(k/32) uint32, word [b][w] bit i = P[32w+i][b]. */
+ldpc_status ldpc_code_copy_H(const ldpc_code *code, uint8_t *dense_mxn);
+ldpc_status ldpc_code_copy_csr(const ldpc_code *code, int32_t *row_ptr, int32_t *col_idx);
+ldpc_status ldpc_code_copy_perm(const ldpc_code *code, int32_t *perm_n);
+ldpc_status ldpc_code_copy_P(const ldpc_code *code, uint32_t *p_packed);
+
+/* Copy the code's device image (graph, permutation, packed P) into the
+ * caller's device buffer d_buf (>= info.device_bytes, 256-byte aligned),
+ * enqueued on `stream`.  d_buf must outlive every encode/decode that uses the
+ * code.  Calling it again re-binds.  May be called before ldpc_make_G (then
+ * only decoding is available) and again after it. */
+ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, void *stream);
+
+void ldpc_code_free(ldpc_code *code);
+const char *ldpc_status_str(ldpc_status s);
+
+/* ---------------------------------------------------------------- hot path */
+
+/* Encode, Eq. 3 in standard form: for every frame,
+ * c[perm[t]] = m_t (t < k) and c[perm[k+b]] = XOR_a m_a P[a][b].
+ * d_info: frames * ceil(k/32) uint32 (packed message bits);
+ * d_cw:   frames * ceil(n/32) uint32 (packed codeword, H column order).
+ * Requires make_G and bind_device after it (else LDPC_ERR_STATE). */
+ldpc_status ldpc_encode(const ldpc_code *code, const uint32_t *d_info, uint32_t *d_cw,
+                        int64_t frames, void *stream);
+
+/* Workspace the chosen decode variant needs for `frames` frames (0 for the
+ * on-chip variants; the large-n variants keep per-frame message state in it). */
+ldpc_status ldpc_decode_workspace_bytes(const ldpc_code *code, int64_t frames,
+                                        const ldpc_decode_opts *opts, size_t *bytes);
+
+/* Batched Sum-Product decoding (flooding schedule of Alg. 1,
+ * P:351-369; batch processing P:542-544; stream processing = frames == 1).
+ *   d_llr:       frames * n float32 channel LLRs R_v (Eq. 4), clamped to +-30
+ *                on load (reading Q7).  16-byte aligned.
+ *   d_bits:      frames * ceil(n/32) uint32: hard decisions z (Eq. 8).
+ *   d_syndrome_ok: frames uint8: 1 iff H z^T = 0 (Eq. 1).
+ *   d_iters:     frames int32: iterations run (max_iter unless early_term).
+ *   d_posterior: nullable; frames * n float32 total LLRs L_v (Eq. 7).
+ *   d_ws/ws_bytes: workspace, >= ldpc_decode_workspace_bytes().
+ * Check update E_cv = (-1)^{d_c} prod sgn(L_v'c) * phi(sum phi(|L_v'c|)),
+ * phi(x) = -ln tanh(x/2) (Eq. 5, reading Q2/Q3), L_v'c clamped to
+ * +-30, |E_cv| <= E_MAX = 2 atanh(1 - 1e-12) (reading Q7).
+ * opts->variant: 0 auto, 1 on-chip team-per-frame, 2 global-state
+ * CTA-per-frame. */
+ldpc_status ldpc_decode(const ldpc_code *code, const float *d_llr, int64_t frames,
+                        const ldpc_decode_opts *opts, uint32_t *d_bits,
+                        uint8_t *d_syndrome_ok, int32_t *d_iters, float *d_posterior,
+                        void *d_ws, size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------- harness helpers */
+
+/* Info bits (reading c4): word w of frame f = lane w%4 of Philox4x32-10 with
+ * key (seed_lo, seed_hi), counter (w/4, f_lo, f_hi, 0); last word masked to k.
+ * Frames frame0 .. frame0+frames-1; d_info: frames * ceil(k/32) uint32. */
+ldpc_status ldpc_gen_info(uint64_t seed, int64_t frame0, int64_t frames, int32_t k,
+                          uint32_t *d_info, void *stream);
+
+/* BPSK (0 -> -1, 1 -> +1) over AWGN of std sigma and the
+ * channel LLR R = fp32(clamp(2y/sigma^2, +-30)) (Eq. 4, reading Q1).  Noise:
+ * Philox counter (v/4, f_lo, f_hi, 1), Box-Muller in fp64 (reading c4).
+ * d_cw: frames * ceil(n/32) uint32; d_llr: frames * n float32. */
+ldpc_status ldpc_channel(const ldpc_code *code, uint64_t seed, int64_t frame0, int64_t frames,
+                         const uint32_t *d_cw, double sigma, float *d_llr, void *stream);
+
+/* Error counters, ACCUMULATED (+=) into d_counters6 (int64[6]):
+ * [0] info-bit errors (decoded bits at perm[0..k) vs d_info), [1] codeword-bit
+ * errors (vs d_cw), [2] frame errors (any info-bit error), [3] undetected
+ * errors (syndrome_ok but some codeword bit wrong), [4] sum of iterations,
+ * [5] frames (SPEC run_ber S:522-530, reading Q14).  Requires make_G. */
+ldpc_status ldpc_count_errors(const ldpc_code *code, const uint32_t *d_info,
+                              const uint32_t *d_bits, const uint32_t *d_cw,
+                              const uint8_t *d_syndrome_ok, const int32_t *d_iters,
+                              int64_t frames, int64_t *d_counters6, void *stream);
+
+/* Diagnostics: y[i] = phi(x[i]) with the decoder's own device phi,
+ * phi(x) = -ln tanh(x/2) for x >= 0 (the log-domain form of Eq. 5's
+ * tanh/atanh pair).  For the exhaustive accuracy sweep in tests.
+ * d_x, d_y: count float32 (device). */
+ldpc_status ldpc_debug_phi(const float *d_x, float *d_y, int64_t count, void *stream);
+
+/* Work partition, Eq. 9 (corrected per S:336, reading Q6):
+ * counts[q] = floor(l/N) + (q < l mod N), displs = exclusive prefix sum.
+ * Used to shard frames across GPUs (one rank per GPU). Host. */
+ldpc_status ldpc_partition(int64_t l, int32_t nproc, int64_t *counts, int64_t *displs);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LDPC_B200_H */

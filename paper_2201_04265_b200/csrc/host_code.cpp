@@ -1,0 +1,375 @@
+// host_code.cpp -- host side of the C ABI: code construction (Gallager H,
+// external CSR), standard-form generator (GF(2) Gauss-Jordan), queries, the
+// device image, and the frame partition.  Independent of oracle/ (shares no
+// code with it); bit-exactness with it is asserted by tests/test_host_vs_oracle.py.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <thread>
+#include <vector>
+
+#include "ldpc_internal.h"
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// SplitMix64 (Steele/Lea/Flood 2014) and an unbiased bounded draw by
+// rejection: r is rejected when r >= 2^64 - (2^64 mod s) (reading Q12).
+struct SplitMix64 {
+    uint64_t s;
+    explicit SplitMix64(uint64_t seed) : s(seed) {}
+    uint64_t next() {
+        s += 0x9E3779B97F4A7C15ULL;
+        uint64_t z = s;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+        return z ^ (z >> 31);
+    }
+    uint64_t below(uint64_t bound) {
+        const uint64_t rem = (~bound + 1) % bound;          // 2^64 mod bound
+        const uint64_t limit = ~rem + 1;                     // 2^64 - rem (0 when rem == 0)
+        for (;;) {
+            uint64_t r = next();
+            if (rem == 0 || r < limit) return r % bound;
+        }
+    }
+};
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+void build_csc(ldpc_code &c) {
+    c.var_ptr.assign(size_t(c.n) + 1, 0);
+    for (int32_t e = 0; e < c.nnz; ++e) c.var_ptr[size_t(c.col_idx[e]) + 1]++;
+    for (int32_t v = 0; v < c.n; ++v) c.var_ptr[size_t(v) + 1] += c.var_ptr[v];
+    c.var_edges.assign(size_t(c.nnz), 0);
+    std::vector<int32_t> cursor(c.var_ptr.begin(), c.var_ptr.end() - 1);
+    for (int32_t chk = 0; chk < c.m; ++chk)            // ascending check order per variable
+        for (int32_t e = c.row_ptr[chk]; e < c.row_ptr[chk + 1]; ++e)
+            c.var_edges[size_t(cursor[c.col_idx[e]]++)] = e;
+    c.max_row_deg = 0;
+    int32_t min_row = c.m ? INT32_MAX : 0;
+    for (int32_t chk = 0; chk < c.m; ++chk) {
+        int32_t d = c.row_ptr[chk + 1] - c.row_ptr[chk];
+        c.max_row_deg = std::max(c.max_row_deg, d);
+        min_row = std::min(min_row, d);
+    }
+    c.max_col_deg = 0;
+    int32_t min_col = c.n ? INT32_MAX : 0;
+    for (int32_t v = 0; v < c.n; ++v) {
+        int32_t d = c.var_ptr[v + 1] - c.var_ptr[v];
+        c.max_col_deg = std::max(c.max_col_deg, d);
+        min_col = std::min(min_col, d);
+    }
+    c.regular_row = (min_row == c.max_row_deg);
+    c.regular_col = (min_col == c.max_col_deg);
+}
+
+unsigned worker_count() {
+    unsigned h = std::thread::hardware_concurrency();
+    return std::max(1u, std::min(h ? h : 1u, 64u));
+}
+
+}  // namespace
+
+namespace ldpc {
+DeviceLayout compute_layout(const ldpc_code &c, bool with_G) {
+    DeviceLayout L;
+    size_t off = 0;
+    L.row_ptr = off;   off = align256(off + sizeof(int32_t) * (size_t(c.m) + 1));
+    L.col_idx = off;   off = align256(off + sizeof(int32_t) * size_t(std::max(c.nnz, 1)));
+    L.var_ptr = off;   off = align256(off + sizeof(int32_t) * (size_t(c.n) + 1));
+    L.var_edges = off; off = align256(off + sizeof(int32_t) * size_t(std::max(c.nnz, 1)));
+    if (with_G) {
+        size_t kw = (size_t(c.k) + 31) / 32;
+        L.perm = off;  off = align256(off + sizeof(int32_t) * size_t(c.n));
+        L.pinv = off;  off = align256(off + sizeof(int32_t) * size_t(c.n));
+        L.pcols = off; off = align256(off + sizeof(uint32_t) * std::max<size_t>(size_t(c.n - c.k) * kw, 1));
+    }
+    L.total = off;
+    return L;
+}
+}  // namespace ldpc
+
+extern "C" {
+
+const char *ldpc_status_str(ldpc_status s) {
+    switch (s) {
+        case LDPC_OK: return "ok";
+        case LDPC_ERR_ARG: return "invalid argument";
+        case LDPC_ERR_NOT_DIVISIBLE: return "wr does not divide n";
+        case LDPC_ERR_NO_INFO_BITS: return "code has no information bits (k == 0)";
+        case LDPC_ERR_DIM: return "dimension mismatch";
+        case LDPC_ERR_STATE: return "call out of order (make_G / bind_device missing)";
+        case LDPC_ERR_UNSUPPORTED: return "unsupported code (degree > 32?)";
+        case LDPC_ERR_CUDA: return "CUDA runtime error";
+        case LDPC_ERR_NOMEM: return "out of host memory";
+    }
+    return "unknown status";
+}
+
+// Gallager band construction, P:37 / P:598.
+ldpc_status ldpc_make_H(int32_t n, int32_t wc, int32_t wr, uint64_t seed, ldpc_code **out) {
+    if (!out) return LDPC_ERR_ARG;
+    *out = nullptr;
+    if (n <= 0 || wc < 1 || wr < 2 || wc >= wr || wr > ldpc::kMaxCheckDegree) return LDPC_ERR_ARG;
+    if (n % wr) return LDPC_ERR_NOT_DIVISIBLE;
+    ldpc_code *c = new (std::nothrow) ldpc_code;
+    if (!c) return LDPC_ERR_NOMEM;
+    try {
+        const int32_t mb = n / wr;
+        c->n = n; c->m = mb * wc; c->nnz = c->m * wr;
+        c->wc = wc; c->wr = wr; c->gallager = 1;
+        c->design_rate = 1.0 - double(wc) / double(wr);
+        c->row_ptr.resize(size_t(c->m) + 1);
+        for (int32_t r = 0; r <= c->m; ++r) c->row_ptr[r] = r * wr;
+        c->col_idx.resize(size_t(c->nnz));
+        std::vector<int32_t> pi(static_cast<size_t>(n));
+        SplitMix64 rng(seed);
+        for (int32_t band = 0; band < wc; ++band) {
+            for (int32_t i = 0; i < n; ++i) pi[i] = i;
+            if (band > 0)
+                for (int32_t i = n - 1; i > 0; --i) {
+                    int32_t j = int32_t(rng.below(uint64_t(i) + 1));
+                    std::swap(pi[i], pi[j]);
+                }
+            // row band*mb + r holds pi[r*wr .. r*wr+wr): edge ids are band*n + position
+            std::copy(pi.begin(), pi.end(), c->col_idx.begin() + size_t(band) * n);
+        }
+        build_csc(*c);
+    } catch (...) {
+        delete c;
+        return LDPC_ERR_NOMEM;
+    }
+    *out = c;
+    return LDPC_OK;
+}
+
+ldpc_status ldpc_code_from_csr(int32_t m, int32_t n, const int32_t *row_ptr, const int32_t *col_idx,
+                               ldpc_code **out) {
+    if (!out) return LDPC_ERR_ARG;
+    *out = nullptr;
+    if (m < 0 || n <= 0 || !row_ptr || (row_ptr[m] > 0 && !col_idx) || row_ptr[0] != 0)
+        return LDPC_ERR_ARG;
+    for (int32_t r = 0; r < m; ++r) {
+        int32_t d = row_ptr[r + 1] - row_ptr[r];
+        if (d < 0) return LDPC_ERR_ARG;
+        if (d > ldpc::kMaxCheckDegree) return LDPC_ERR_UNSUPPORTED;
+    }
+    std::vector<uint8_t> seen(static_cast<size_t>(n), 0);
+    for (int32_t r = 0; r < m; ++r) {
+        for (int32_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
+            int32_t v = col_idx[e];
+            if (v < 0 || v >= n || seen[v]) {
+                for (int32_t q = row_ptr[r]; q < e; ++q) seen[col_idx[q]] = 0;
+                return LDPC_ERR_ARG;
+            }
+            seen[v] = 1;
+        }
+        for (int32_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) seen[col_idx[e]] = 0;
+    }
+    ldpc_code *c = new (std::nothrow) ldpc_code;
+    if (!c) return LDPC_ERR_NOMEM;
+    try {
+        c->n = n; c->m = m; c->nnz = row_ptr[m];
+        c->row_ptr.assign(row_ptr, row_ptr + m + 1);
+        c->col_idx.assign(col_idx, col_idx + c->nnz);
+        c->design_rate = 1.0 - double(m) / double(n);
+        build_csc(*c);
+    } catch (...) {
+        delete c;
+        return LDPC_ERR_NOMEM;
+    }
+    *out = c;
+    return LDPC_OK;
+}
+
+// Standard-form generator, Eq. 2-3; reading Q13.
+// Bit-packed rows (64 columns per word); the pivot search is sequential, the
+// elimination of column j from all other rows is split across host threads.
+ldpc_status ldpc_make_G(ldpc_code *code) {
+    if (!code) return LDPC_ERR_ARG;
+    ldpc_code &c = *code;
+    const int32_t n = c.n, m = c.m;
+    const size_t W = (size_t(n) + 63) / 64;
+    std::vector<uint64_t> M;
+    try {
+        M.assign(size_t(m) * W, 0);
+    } catch (...) {
+        return LDPC_ERR_NOMEM;
+    }
+    for (int32_t r = 0; r < m; ++r)
+        for (int32_t e = c.row_ptr[r]; e < c.row_ptr[r + 1]; ++e) {
+            int32_t v = c.col_idx[e];
+            M[size_t(r) * W + size_t(v >> 6)] ^= uint64_t(1) << (v & 63);
+        }
+    std::vector<int32_t> pivot_row(static_cast<size_t>(n), -1);
+    const unsigned T = worker_count();
+    int32_t rank = 0;
+    std::vector<int32_t> targets;
+    targets.reserve(size_t(m));
+    for (int32_t j = n - 1; j >= 0 && rank < m; --j) {
+        const size_t w = size_t(j >> 6);
+        const uint64_t bit = uint64_t(1) << (j & 63);
+        int32_t p = -1;
+        for (int32_t r = rank; r < m; ++r)
+            if (M[size_t(r) * W + w] & bit) { p = r; break; }
+        if (p < 0) continue;
+        if (p != rank)
+            std::swap_ranges(M.begin() + ptrdiff_t(size_t(p) * W), M.begin() + ptrdiff_t(size_t(p) * W + W),
+                             M.begin() + ptrdiff_t(size_t(rank) * W));
+        targets.clear();
+        for (int32_t r = 0; r < m; ++r)
+            if (r != rank && (M[size_t(r) * W + w] & bit)) targets.push_back(r);
+        const uint64_t *src = M.data() + size_t(rank) * W;
+        auto work = [&](size_t lo, size_t hi) {
+            for (size_t t = lo; t < hi; ++t) {
+                uint64_t *dst = M.data() + size_t(targets[t]) * W;
+                for (size_t q = 0; q < W; ++q) dst[q] ^= src[q];
+            }
+        };
+        const size_t ntar = targets.size();
+        if (ntar * W < (size_t(1) << 16) || T == 1) {
+            work(0, ntar);
+        } else {
+            std::vector<std::thread> pool;
+            size_t chunk = (ntar + T - 1) / T;
+            for (unsigned t = 0; t < T; ++t) {
+                size_t lo = size_t(t) * chunk, hi = std::min(ntar, lo + chunk);
+                if (lo < hi) pool.emplace_back(work, lo, hi);
+            }
+            for (auto &th : pool) th.join();
+        }
+        pivot_row[size_t(j)] = rank;
+        ++rank;
+    }
+    const int32_t k = n - rank;
+    if (k == 0) return LDPC_ERR_NO_INFO_BITS;
+    try {
+        c.perm.resize(size_t(n));
+        int32_t nf = 0, np = 0;
+        for (int32_t j = 0; j < n; ++j)
+            if (pivot_row[size_t(j)] < 0) c.perm[size_t(nf++)] = j;
+        for (int32_t j = 0; j < n; ++j)
+            if (pivot_row[size_t(j)] >= 0) c.perm[size_t(k + np++)] = j;
+        c.pinv.resize(size_t(n));
+        for (int32_t t = 0; t < n; ++t) c.pinv[size_t(c.perm[size_t(t)])] = t;
+        const size_t kw = (size_t(k) + 31) / 32;
+        c.pcols.assign(size_t(n - k) * kw, 0u);
+        for (int32_t b = 0; b < n - k; ++b) {
+            const uint64_t *row = M.data() + size_t(pivot_row[size_t(c.perm[size_t(k + b)])]) * W;
+            uint32_t *col = c.pcols.data() + size_t(b) * kw;
+            for (int32_t a = 0; a < k; ++a) {
+                int32_t fa = c.perm[size_t(a)];
+                if ((row[fa >> 6] >> (fa & 63)) & 1u) col[a >> 5] |= 1u << (a & 31);
+            }
+        }
+    } catch (...) {
+        return LDPC_ERR_NOMEM;
+    }
+    c.rank = rank;
+    c.k = k;
+    c.has_G = true;
+    c.bound_G = false;   // the device image (if any) predates G
+    return LDPC_OK;
+}
+
+ldpc_status ldpc_code_query(const ldpc_code *code, ldpc_code_info *info) {
+    if (!code || !info) return LDPC_ERR_ARG;
+    info->n = code->n; info->m = code->m; info->k = code->k; info->rank = code->rank;
+    info->nnz = code->nnz; info->max_row_deg = code->max_row_deg; info->max_col_deg = code->max_col_deg;
+    info->wc = code->wc; info->wr = code->wr; info->gallager = code->gallager;
+    info->design_rate = code->design_rate;
+    info->device_bytes = ldpc::compute_layout(*code, code->has_G).total;
+    return LDPC_OK;
+}
+
+ldpc_status ldpc_code_copy_H(const ldpc_code *code, uint8_t *dense) {
+    if (!code || !dense) return LDPC_ERR_ARG;
+    std::memset(dense, 0, size_t(code->m) * size_t(code->n));
+    for (int32_t r = 0; r < code->m; ++r)
+        for (int32_t e = code->row_ptr[r]; e < code->row_ptr[r + 1]; ++e)
+            dense[size_t(r) * code->n + size_t(code->col_idx[e])] = 1;
+    return LDPC_OK;
+}
+
+ldpc_status ldpc_code_copy_csr(const ldpc_code *code, int32_t *row_ptr, int32_t *col_idx) {
+    if (!code || !row_ptr || (!col_idx && code->nnz)) return LDPC_ERR_ARG;
+    std::copy(code->row_ptr.begin(), code->row_ptr.end(), row_ptr);
+    std::copy(code->col_idx.begin(), code->col_idx.end(), col_idx);
+    return LDPC_OK;
+}
+
+ldpc_status ldpc_code_copy_perm(const ldpc_code *code, int32_t *perm) {
+    if (!code || !perm) return LDPC_ERR_ARG;
+    if (!code->has_G) return LDPC_ERR_STATE;
+    std::copy(code->perm.begin(), code->perm.end(), perm);
+    return LDPC_OK;
+}
+
+ldpc_status ldpc_code_copy_P(const ldpc_code *code, uint32_t *p) {
+    if (!code || !p) return LDPC_ERR_ARG;
+    if (!code->has_G) return LDPC_ERR_STATE;
+    std::copy(code->pcols.begin(), code->pcols.end(), p);
+    return LDPC_OK;
+}
+
+ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, void *stream) {
+    if (!code || !d_buf) return LDPC_ERR_ARG;
+    if (reinterpret_cast<uintptr_t>(d_buf) & 255u) return LDPC_ERR_ARG;
+    ldpc::DeviceLayout L = ldpc::compute_layout(*code, code->has_G);
+    if (bytes < L.total) return LDPC_ERR_ARG;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    char *base = static_cast<char *>(d_buf);
+    auto put = [&](size_t off, const void *src, size_t nbytes) -> bool {
+        if (nbytes == 0) return true;
+        return cudaMemcpyAsync(base + off, src, nbytes, cudaMemcpyHostToDevice, s) == cudaSuccess;
+    };
+    bool ok = put(L.row_ptr, code->row_ptr.data(), sizeof(int32_t) * code->row_ptr.size()) &&
+              put(L.col_idx, code->col_idx.data(), sizeof(int32_t) * code->col_idx.size()) &&
+              put(L.var_ptr, code->var_ptr.data(), sizeof(int32_t) * code->var_ptr.size()) &&
+              put(L.var_edges, code->var_edges.data(), sizeof(int32_t) * code->var_edges.size());
+    if (ok && code->has_G)
+        ok = put(L.perm, code->perm.data(), sizeof(int32_t) * code->perm.size()) &&
+             put(L.pinv, code->pinv.data(), sizeof(int32_t) * code->pinv.size()) &&
+             put(L.pcols, code->pcols.data(), sizeof(uint32_t) * code->pcols.size());
+    // The host vectors are pageable: cudaMemcpyAsync from pageable memory is
+    // staged synchronously, so they may be reused as soon as the call returns.
+    if (!ok) return LDPC_ERR_CUDA;
+    code->d_buf = d_buf;
+    code->d_bytes = bytes;
+    code->layout = L;
+    code->bound_G = code->has_G;
+    ldpc::DeviceCode &D = code->dev;
+    D.n = code->n; D.m = code->m; D.k = code->has_G ? code->k : 0; D.nnz = code->nnz;
+    D.max_row_deg = code->max_row_deg; D.max_col_deg = code->max_col_deg;
+    D.regular_row = code->regular_row; D.regular_col = code->regular_col;
+    D.kw = code->has_G ? (code->k + 31) / 32 : 0;
+    D.nw = (code->n + 31) / 32;
+    D.row_ptr = reinterpret_cast<const int32_t *>(base + L.row_ptr);
+    D.col_idx = reinterpret_cast<const int32_t *>(base + L.col_idx);
+    D.var_ptr = reinterpret_cast<const int32_t *>(base + L.var_ptr);
+    D.var_edges = reinterpret_cast<const int32_t *>(base + L.var_edges);
+    D.perm = code->has_G ? reinterpret_cast<const int32_t *>(base + L.perm) : nullptr;
+    D.pinv = code->has_G ? reinterpret_cast<const int32_t *>(base + L.pinv) : nullptr;
+    D.pcols = code->has_G ? reinterpret_cast<const uint32_t *>(base + L.pcols) : nullptr;
+    return LDPC_OK;
+}
+
+void ldpc_code_free(ldpc_code *code) { delete code; }
+
+// Eq. 9, corrected (reading Q6).
+ldpc_status ldpc_partition(int64_t l, int32_t nproc, int64_t *counts, int64_t *displs) {
+    if (l < 0 || nproc < 1 || !counts || !displs) return LDPC_ERR_ARG;
+    const int64_t base = l / nproc, extra = l % nproc;
+    int64_t off = 0;
+    for (int32_t q = 0; q < nproc; ++q) {
+        counts[q] = base + (q < extra ? 1 : 0);
+        displs[q] = off;
+        off += counts[q];
+    }
+    return LDPC_OK;
+}
+
+}  // extern "C"

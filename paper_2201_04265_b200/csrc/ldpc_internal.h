@@ -1,0 +1,71 @@
+// ldpc_internal.h -- library-internal structures shared by the host code
+// (host_code.cpp) and the CUDA kernels (*.cu).  Not part of the ABI; the
+// oracle never includes it.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+#include "../../include/ldpc.h"
+
+namespace ldpc {
+
+constexpr int kMaxCheckDegree = 32;   // generic-kernel limit (register arrays)
+constexpr float kLlrClamp = 30.0f;    // reading Q7: R and L_vc clamped to +-30
+// reading Q7: |E_cv| <= 2 atanh(1 - 1e-12) = ln(2e12 - 1) = 28.32416830...
+constexpr float kEMax = 28.3241683f;
+
+// Offsets (bytes) of the arrays inside the caller's device buffer.
+struct DeviceLayout {
+    size_t row_ptr = 0;    // int32 [m+1]       check -> first edge (CSR)
+    size_t col_idx = 0;    // int32 [nnz]       edge  -> variable
+    size_t var_ptr = 0;    // int32 [n+1]       variable -> first slot in var_edges
+    size_t var_edges = 0;  // int32 [nnz]       edges of each variable, ascending check
+    size_t perm = 0;       // int32 [n]         (after make_G)
+    size_t pinv = 0;       // int32 [n]         inverse of perm: position of column v in [m | mP]
+    size_t pcols = 0;      // uint32 [(n-k)*kw] P packed by parity column
+    size_t total = 0;
+};
+
+// Plain-old-data view of a bound code, passed by value to kernels.
+struct DeviceCode {
+    int32_t n, m, k, nnz;
+    int32_t max_row_deg, max_col_deg;
+    int32_t regular_row;   // every check has degree max_row_deg
+    int32_t regular_col;   // every variable has degree max_col_deg
+    int32_t kw, nw;        // ceil(k/32), ceil(n/32)
+    const int32_t *row_ptr;
+    const int32_t *col_idx;
+    const int32_t *var_ptr;
+    const int32_t *var_edges;
+    const int32_t *perm;
+    const int32_t *pinv;
+    const uint32_t *pcols;
+};
+
+}  // namespace ldpc
+
+struct ldpc_code {
+    int32_t n = 0, m = 0, k = -1, rank = -1, nnz = 0;
+    int32_t max_row_deg = 0, max_col_deg = 0;
+    int32_t wc = 0, wr = 0, gallager = 0;
+    int32_t regular_row = 0, regular_col = 0;
+    double design_rate = 0.0;
+    std::vector<int32_t> row_ptr, col_idx;     // H as CSR, check-major edge ids
+    std::vector<int32_t> var_ptr, var_edges;   // CSC view: edge ids per variable
+    std::vector<int32_t> perm;                 // [free cols asc, pivot cols asc]
+    std::vector<int32_t> pinv;                 // pinv[perm[t]] = t
+    std::vector<uint32_t> pcols;               // (n-k) x kw
+    bool has_G = false;
+    // device binding
+    void *d_buf = nullptr;
+    size_t d_bytes = 0;
+    bool bound_G = false;
+    ldpc::DeviceLayout layout;
+    ldpc::DeviceCode dev{};
+};
+
+namespace ldpc {
+DeviceLayout compute_layout(const ldpc_code &c, bool with_G);
+}
