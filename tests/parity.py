@@ -12,7 +12,10 @@ Rule:
     1e-3 absolute or 1e-4 relative; hard decisions agree except where
     |L_oracle| < 1e-3; syndrome flags agree; iteration counts agree.
  4. Ill-conditioned frames are counted and reported; their hard decisions
-    are gated only where both oracle runs agree in sign with |L| >= 1e-3.
+    are gated only on STABLE bits: both oracle runs agree in sign and |L|
+    exceeds max(1e-3, 10 s_f), s_f = the frame's measured sensitivity
+    max|L1 - L2| (a bit whose margin is within the frame's own chaos scale is
+    not decided by the algorithm but by rounding).
 """
 from __future__ import annotations
 
@@ -89,7 +92,9 @@ def compare(O, code, R: np.ndarray, gpu_L: np.ndarray, gpu_z: np.ndarray, gpu_sy
     for f in range(R.shape[0]):
         if ill[f]:
             max_ex = max(max_ex, float(err[f].max()))
-            stable = (np.sign(L1[f]) == np.sign(L2[f])) & (np.abs(L1[f]) >= 1e-3) & (np.abs(L2[f]) >= 1e-3)
+            s_f = float(np.max(np.abs(np.clip(L1[f], -CLIP, CLIP) - np.clip(L2[f], -CLIP, CLIP))))
+            margin = max(1e-3, 10.0 * s_f)
+            stable = (np.sign(L1[f]) == np.sign(L2[f])) & (np.abs(L1[f]) >= margin) & (np.abs(L2[f]) >= margin)
             if np.any(z_diff[f] & stable):
                 failures.append((f, "hard decision (ill-conditioned, stable bits)"))
             continue
