@@ -81,6 +81,11 @@ DeviceLayout compute_layout(const ldpc_code &c, bool with_G) {
     L.col_idx = off;   off = align256(off + sizeof(int32_t) * size_t(std::max(c.nnz, 1)));
     L.var_ptr = off;   off = align256(off + sizeof(int32_t) * (size_t(c.n) + 1));
     L.var_edges = off; off = align256(off + sizeof(int32_t) * size_t(std::max(c.nnz, 1)));
+    if (c.gallager && c.wc >= 2) {
+        const size_t nb = size_t(c.wc - 1) * size_t(c.n);
+        L.band_lidx = off; off = align256(off + sizeof(int32_t) * nb);
+        L.band_vpos = off; off = align256(off + sizeof(int32_t) * nb);
+    }
     if (with_G) {
         size_t kw = (size_t(c.k) + 31) / 32;
         L.perm = off;  off = align256(off + sizeof(int32_t) * size_t(c.n));
@@ -330,6 +335,23 @@ ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, vo
               put(L.col_idx, code->col_idx.data(), sizeof(int32_t) * code->col_idx.size()) &&
               put(L.var_ptr, code->var_ptr.data(), sizeof(int32_t) * code->var_ptr.size()) &&
               put(L.var_edges, code->var_edges.data(), sizeof(int32_t) * code->var_edges.size());
+    std::vector<int32_t> lidx, vpos;
+    if (ok && code->gallager && code->wc >= 2) {
+        // Band view: edge (band b >= 1, position p) of row b*mb + p/wr is CSR edge
+        // b*n + p (ldpc_make_H orders rows band-major, slots in pi_b order).
+        const int32_t n = code->n, wc = code->wc;
+        const size_t lbase = ldpc::band_L_byte_offset(n, wc);
+        lidx.resize(size_t(wc - 1) * size_t(n));
+        vpos.resize(size_t(wc - 1) * size_t(n));
+        for (int32_t b = 1; b < wc; ++b)
+            for (int32_t p = 0; p < n; ++p) {
+                const int32_t v = code->col_idx[size_t(b) * n + p];
+                lidx[size_t(b - 1) * n + p] = int32_t(lbase + 4 * size_t(v));
+                vpos[size_t(v) * (wc - 1) + (b - 1)] = int32_t(4 * (size_t(b - 1) * n + p));
+            }
+        ok = put(L.band_lidx, lidx.data(), sizeof(int32_t) * lidx.size()) &&
+             put(L.band_vpos, vpos.data(), sizeof(int32_t) * vpos.size());
+    }
     if (ok && code->has_G)
         ok = put(L.perm, code->perm.data(), sizeof(int32_t) * code->perm.size()) &&
              put(L.pinv, code->pinv.data(), sizeof(int32_t) * code->pinv.size()) &&
@@ -353,6 +375,10 @@ ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, vo
     D.var_edges = reinterpret_cast<const int32_t *>(base + L.var_edges);
     D.perm = code->has_G ? reinterpret_cast<const int32_t *>(base + L.perm) : nullptr;
     D.pinv = code->has_G ? reinterpret_cast<const int32_t *>(base + L.pinv) : nullptr;
+    D.gallager = code->gallager; D.wc = code->wc; D.wr = code->wr;
+    D.mb = code->gallager ? code->n / code->wr : 0;
+    D.band_lidx = (code->gallager && code->wc >= 2) ? reinterpret_cast<const int32_t *>(base + L.band_lidx) : nullptr;
+    D.band_vpos = (code->gallager && code->wc >= 2) ? reinterpret_cast<const int32_t *>(base + L.band_vpos) : nullptr;
     D.pcols = code->has_G ? reinterpret_cast<const uint32_t *>(base + L.pcols) : nullptr;
     return LDPC_OK;
 }

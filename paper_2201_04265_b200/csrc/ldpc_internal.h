@@ -25,6 +25,9 @@ struct DeviceLayout {
     size_t perm = 0;       // int32 [n]         (after make_G)
     size_t pinv = 0;       // int32 [n]         inverse of perm: position of column v in [m | mP]
     size_t pcols = 0;      // uint32 [(n-k)*kw] P packed by parity column
+    // Gallager band view (ldpc_make_H codes only), used by the band kernel:
+    size_t band_lidx = 0;  // int32 [(wc-1)*n]  edge (band b>=1, position p) -> byte offset of L[pi_b[p]]
+    size_t band_vpos = 0;  // int32 [n*(wc-1)]  variable v, band b>=1 -> byte offset of its E in E_hi
     size_t total = 0;
 };
 
@@ -42,7 +45,15 @@ struct DeviceCode {
     const int32_t *perm;
     const int32_t *pinv;
     const uint32_t *pcols;
+    int32_t gallager, wc, wr, mb;   // band structure (mb = n / wr rows per band)
+    const int32_t *band_lidx;
+    const int32_t *band_vpos;
 };
+
+// Shared-memory image of one frame in the band kernel (floats):
+//   E_hi[(wc-1) n] (bands 1.., check-major: band b row r slot j at (b-1) n + r wr + j)
+//   L[n]  (posterior, log2 units)      R[n] (channel LLR, log2 units; optional)
+inline size_t band_L_byte_offset(int32_t n, int32_t wc) { return size_t(wc - 1) * size_t(n) * 4; }
 
 }  // namespace ldpc
 
@@ -68,4 +79,20 @@ struct ldpc_code {
 
 namespace ldpc {
 DeviceLayout compute_layout(const ldpc_code &c, bool with_G);
-}
+
+// Launch plan of the Gallager band kernel (spa_band.cu).
+struct BandPlan {
+    void *kernel = nullptr;
+    int threads = 0;
+    int grid = 0;
+    size_t smem = 0;
+    bool r_in_smem = false;
+    size_t ws_bytes = 0;
+};
+// false when the code is not eligible (not from ldpc_make_H, unsupported
+// (wc, wr), n % 4 != 0, or the frame does not fit one SM's shared memory).
+bool band_plan(const ldpc_code &c, int64_t frames, bool et, BandPlan &p);
+ldpc_status band_launch(const ldpc_code &c, const BandPlan &p, const float *llr, int64_t frames,
+                        const ldpc_decode_opts &o, uint32_t *bits, uint8_t *syn, int32_t *iters, float *post,
+                        void *ws, size_t ws_bytes, void *stream);
+}  // namespace ldpc

@@ -1,0 +1,391 @@
+// spa_band.cu -- the Sum-Product decoder specialised for regular Gallager
+// codes built by ldpc_make_H (band construction S:52): the hot path of
+// every BASELINE.json config.  Same algorithm and schedule as spa_decode.cu
+// (Eqs. 4-8; flooding, Alg. 1); the structure of H is
+// used to cut instructions and shared-memory traffic:
+//
+//  * Band 0 row r holds variables [r wr, (r+1) wr): the thread that owns
+//    band-0 row r keeps that row's E_cv in REGISTERS across iterations, reads
+//    the row's L_v as contiguous vectors, and performs the variable-node update
+//    (Eq. 7) for exactly those wr variables.  Only the E of bands 1..wc-1 and
+//    L (and R when it fits) live in shared memory -- which is what lets an
+//    n = 16200 frame decode inside one SM (2n + n floats = 194 KB).
+//  * Graph indices are pre-scaled byte offsets into the frame's shared-memory
+//    image (DeviceLayout::band_lidx / band_vpos), read with vector loads.
+//  * All LLRs are carried in log2 units (L' = L log2 e): phi becomes
+//    psi(y) = log2(e) phi(y ln 2), still self-inverse, and e^-x becomes a bare
+//    ex2 on the SFU.  R is scaled on ingest, posteriors rescaled on output.
+//  * One CTA decodes one frame at a time (persistent grid); frames are taken
+//    from a global atomic counter, so early-terminating frames free their CTA
+//    immediately.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "ldpc_internal.h"
+
+namespace ldpc {
+namespace {
+
+constexpr float kL2E = 1.44269504088896341f;
+constexpr float kLn2 = 0.693147180559945309f;
+constexpr float kClampB = 43.2808512f;    // 30 log2(e)            (reading Q7)
+constexpr float kEMaxB = 40.86313714f;    // log2(2e12 - 1) = E_MAX log2(e)
+// psi(y) = log2(e) phi(y ln2), y >= 0:
+//   y <= 1.8033688: psi = C1 - lg2(y) + y^2 q(y^2)     (one lg2)
+//   y >  1.8033688: psi = t h(t^2),  t = 2^-y          (one ex2)
+constexpr float kSplitB = 1.8033688f;
+constexpr float kC1 = 1.528766373f;
+constexpr float kQ0 = 0.0577617388f, kQ1 = -0.00161740689f, kQ2 = 5.33304814e-05f, kQ3 = -1.50169545e-06f;
+constexpr float kH0 = 2.88539008f, kH1 = 0.961820197f, kH2 = 0.574983425f, kH3 = 0.461572595f;
+
+__device__ __forceinline__ float ex2a(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float lg2a(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float psi(float y) {
+    const float s = y * y;
+    const float q = fmaf(fmaf(fmaf(kQ3, s, kQ2), s, kQ1), s, kQ0);
+    const float small = fmaf(s, q, kC1) - lg2a(y);
+    const float t = ex2a(-y);
+    const float u = t * t;
+    const float h = fmaf(fmaf(fmaf(kH3, u, kH2), u, kH1), u, kH0);
+    const float large = t * h;
+    return y > kSplitB ? large : small;
+}
+
+// Check-node update of one row (Eq. 5, readings Q2/Q3/Q7) in log2 units.
+// x[j] = L'_v - E'_cv (not yet clamped); e[j] <- new E'_cv.
+template <int D>
+__device__ __forceinline__ void check_row(const float (&x)[D], float (&e)[D]) {
+    float f[D];
+    uint32_t sx = (D & 1) ? 0x80000000u : 0u;     // (-1)^{d_c}
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        sx ^= __float_as_uint(x[j]);
+        f[j] = psi(fminf(fabsf(x[j]), kClampB));
+    }
+    float ex[D];
+    float acc = 0.0f;
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        ex[j] = acc;
+        acc += f[j];
+    }
+    acc = 0.0f;
+#pragma unroll
+    for (int j = D - 1; j >= 0; --j) {
+        ex[j] += acc;
+        acc += f[j];
+    }
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        const float mag = fminf(psi(ex[j]), kEMaxB);
+        const uint32_t sgn = (sx ^ __float_as_uint(x[j])) & 0x80000000u;
+        e[j] = __uint_as_float(__float_as_uint(mag) | sgn);
+    }
+}
+
+template <int D>
+__device__ __forceinline__ void lds_row(const char *smem, uint32_t byte_off, float (&o)[D]) {
+    const float *p = reinterpret_cast<const float *>(smem + byte_off);
+    if constexpr (D % 4 == 0) {
+#pragma unroll
+        for (int j = 0; j < D; j += 4) {
+            float4 t = *reinterpret_cast<const float4 *>(p + j);
+            o[j] = t.x; o[j + 1] = t.y; o[j + 2] = t.z; o[j + 3] = t.w;
+        }
+    } else if constexpr (D % 2 == 0) {
+#pragma unroll
+        for (int j = 0; j < D; j += 2) {
+            float2 t = *reinterpret_cast<const float2 *>(p + j);
+            o[j] = t.x; o[j + 1] = t.y;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < D; ++j) o[j] = p[j];
+    }
+}
+template <int D>
+__device__ __forceinline__ void sts_row(char *smem, uint32_t byte_off, const float (&o)[D]) {
+    float *p = reinterpret_cast<float *>(smem + byte_off);
+    if constexpr (D % 4 == 0) {
+#pragma unroll
+        for (int j = 0; j < D; j += 4) *reinterpret_cast<float4 *>(p + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
+    } else if constexpr (D % 2 == 0) {
+#pragma unroll
+        for (int j = 0; j < D; j += 2) *reinterpret_cast<float2 *>(p + j) = make_float2(o[j], o[j + 1]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < D; ++j) p[j] = o[j];
+    }
+}
+template <int D>
+__device__ __forceinline__ void ldg_idx(const int32_t *p, int32_t (&o)[D]) {
+    if constexpr (D % 4 == 0) {
+#pragma unroll
+        for (int j = 0; j < D; j += 4) {
+            int4 t = __ldg(reinterpret_cast<const int4 *>(p + j));
+            o[j] = t.x; o[j + 1] = t.y; o[j + 2] = t.z; o[j + 3] = t.w;
+        }
+    } else if constexpr (D % 2 == 0) {
+#pragma unroll
+        for (int j = 0; j < D; j += 2) {
+            int2 t = __ldg(reinterpret_cast<const int2 *>(p + j));
+            o[j] = t.x; o[j + 1] = t.y;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < D; ++j) o[j] = __ldg(p + j);
+    }
+}
+
+struct BandArgs {
+    DeviceCode code;
+    const float *llr;
+    int64_t frames;
+    int32_t max_iter;
+    int32_t early_term;
+    uint32_t *bits;
+    uint8_t *syn_ok;
+    int32_t *iters;
+    float *posterior;
+    unsigned long long *frame_counter;   // zeroed before launch
+    float *r_global;                     // R' per CTA slot when R does not fit in smem
+    int32_t r_in_smem;
+};
+
+__device__ __forceinline__ bool cta_sync_or(bool p) { return __syncthreads_or(p ? 1 : 0) != 0; }
+
+// WR: row weight, WC: column weight (bands), B0: max band-0 rows per thread.
+template <int WR, int WC, int B0, bool ET>
+__global__ void __launch_bounds__(1024, 1) band_kernel(const BandArgs a) {
+    extern __shared__ __align__(16) char smem[];
+    __shared__ long long s_frame;
+    const DeviceCode &code = a.code;
+    const int n = code.n, mb = code.mb;
+    const int T = blockDim.x, tt = threadIdx.x;
+    constexpr int NB = WC - 1;          // bands held in shared memory
+    constexpr int B1 = NB * B0;         // max rows of bands >= 1 per thread
+    const uint32_t lbase = uint32_t(NB) * uint32_t(n) * 4u;
+    const uint32_t rbase = lbase + uint32_t(n) * 4u;
+    float *Ls = reinterpret_cast<float *>(smem + lbase);
+    float *Rs = a.r_in_smem ? reinterpret_cast<float *>(smem + rbase) : a.r_global + size_t(blockIdx.x) * n;
+    const int32_t *lidx = code.band_lidx;
+    const int32_t *vpos = code.band_vpos;
+
+    for (;;) {
+        if (tt == 0) s_frame = (long long)atomicAdd(a.frame_counter, 1ull);
+        __syncthreads();
+        const long long f = s_frame;
+        if (f >= a.frames) break;
+
+        // a1/a2: ingest R (clamped +-30, log2 units), L = R, E = 0
+        const float *src = a.llr + f * (long long)n;
+        for (int v4 = tt; v4 < (n >> 2); v4 += T) {
+            float4 r = __ldg(reinterpret_cast<const float4 *>(src) + v4);
+            r.x = fminf(fmaxf(r.x, -30.0f), 30.0f) * kL2E;
+            r.y = fminf(fmaxf(r.y, -30.0f), 30.0f) * kL2E;
+            r.z = fminf(fmaxf(r.z, -30.0f), 30.0f) * kL2E;
+            r.w = fminf(fmaxf(r.w, -30.0f), 30.0f) * kL2E;
+            reinterpret_cast<float4 *>(Rs)[v4] = r;
+            reinterpret_cast<float4 *>(Ls)[v4] = r;
+        }
+        for (int i = tt; i < (NB * n) >> 2; i += T)
+            reinterpret_cast<float4 *>(smem)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        float e0[B0][WR];
+#pragma unroll
+        for (int k = 0; k < B0; ++k)
+#pragma unroll
+            for (int j = 0; j < WR; ++j) e0[k][j] = 0.0f;
+        __syncthreads();
+
+        int32_t iters = a.max_iter;
+        bool stopped = false;
+        for (int t = 1; t <= a.max_iter; ++t) {
+            // ---- a3: check-node phase (and syndrome of z^{t-1} when ET)
+            uint32_t synd = 0;
+#pragma unroll
+            for (int k = 0; k < B0; ++k) {
+                const int r = tt + k * T;
+                if (r < mb) {
+                    float lv[WR], x[WR];
+                    lds_row<WR>(smem, lbase + uint32_t(r) * WR * 4u, lv);
+#pragma unroll
+                    for (int j = 0; j < WR; ++j) {
+                        x[j] = lv[j] - e0[k][j];
+                        if (ET) synd ^= (lv[j] >= 0.0f) ? 1u : 0u;
+                    }
+                    check_row<WR>(x, e0[k]);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < B1; ++k) {
+                const int r = tt + k * T;
+                if (r < NB * mb) {
+                    int32_t li[WR];
+                    float e[WR], x[WR];
+                    ldg_idx<WR>(lidx + size_t(r) * WR, li);
+                    lds_row<WR>(smem, uint32_t(r) * WR * 4u, e);
+#pragma unroll
+                    for (int j = 0; j < WR; ++j) {
+                        const float lv = *reinterpret_cast<const float *>(smem + li[j]);
+                        x[j] = lv - e[j];
+                        if (ET) synd ^= (lv >= 0.0f) ? 1u : 0u;
+                    }
+                    check_row<WR>(x, e);
+                    sts_row<WR>(smem, uint32_t(r) * WR * 4u, e);
+                }
+            }
+            if (ET) {
+                const bool any = cta_sync_or(synd != 0);
+                if (t > 1 && !any) {      // z^{t-1} has zero syndrome: stop (reading c6)
+                    iters = t - 1;
+                    stopped = true;
+                    break;
+                }
+            } else {
+                __syncthreads();
+            }
+            // ---- a4/a5: variable-node phase, Eq. 7 (owners of band-0 rows)
+#pragma unroll
+            for (int k = 0; k < B0; ++k) {
+                const int r = tt + k * T;
+                if (r < mb) {
+                    float rv[WR], lv[WR];
+                    int32_t vp[WR * NB];
+                    lds_row<WR>(reinterpret_cast<const char *>(Rs), uint32_t(r) * WR * 4u, rv);
+                    ldg_idx<WR * NB>(vpos + size_t(r) * WR * NB, vp);
+#pragma unroll
+                    for (int j = 0; j < WR; ++j) {
+                        float s = rv[j] + e0[k][j];
+#pragma unroll
+                        for (int b = 0; b < NB; ++b) s += *reinterpret_cast<const float *>(smem + vp[j * NB + b]);
+                        lv[j] = s;
+                    }
+                    sts_row<WR>(smem, lbase + uint32_t(r) * WR * 4u, lv);
+                }
+            }
+            __syncthreads();
+        }
+        // ---- a7: final syndrome when the loop ran to max_iter
+        bool ok = stopped;
+        if (!stopped) {
+            uint32_t synd = 0;
+            for (int r = tt; r < mb; r += T)
+                for (int j = 0; j < WR; ++j) synd ^= (Ls[r * WR + j] >= 0.0f) ? 1u : 0u;
+            for (int r = tt; r < NB * mb; r += T)
+                for (int j = 0; j < WR; ++j)
+                    synd ^= (*reinterpret_cast<const float *>(smem + __ldg(lidx + size_t(r) * WR + j)) >= 0.0f) ? 1u : 0u;
+            ok = !cta_sync_or(synd != 0);
+        }
+        // ---- a6/a8: hard decisions (Eq. 8) packed by ballot, flags, posteriors
+        const int nw = code.nw;
+        uint32_t *bits = a.bits + f * (long long)nw;
+        for (int v = tt; v < nw * 32; v += T) {
+            const bool z = (v < n) ? (Ls[v] >= 0.0f) : false;
+            const uint32_t word = __ballot_sync(0xffffffffu, z);
+            if ((tt & 31) == 0) bits[v >> 5] = word;
+        }
+        if (a.posterior) {
+            float *dst = a.posterior + f * (long long)n;
+            for (int v = tt; v < n; v += T) dst[v] = Ls[v] * kLn2;
+        }
+        if (tt == 0) {
+            a.syn_ok[f] = ok ? 1 : 0;
+            a.iters[f] = iters;
+        }
+        __syncthreads();
+    }
+}
+
+template <int WR, int WC, int B0>
+void *pick_et(bool et) {
+    return et ? reinterpret_cast<void *>(&band_kernel<WR, WC, B0, true>)
+              : reinterpret_cast<void *>(&band_kernel<WR, WC, B0, false>);
+}
+
+template <int WR, int WC>
+void *pick_b0(int b0, bool et) {
+    switch (b0) {
+        case 1: return pick_et<WR, WC, 1>(et);
+        case 2: return pick_et<WR, WC, 2>(et);
+        case 3: return pick_et<WR, WC, 3>(et);
+        case 4: return pick_et<WR, WC, 4>(et);
+    }
+    return nullptr;
+}
+
+void *pick_band_kernel(int wr, int wc, int b0, bool et) {
+    if (wc != 3) return nullptr;
+    switch (wr) {
+        case 4: return pick_b0<4, 3>(b0, et);
+        case 6: return pick_b0<6, 3>(b0, et);
+        case 12: return pick_b0<12, 3>(b0, et);
+    }
+    return nullptr;
+}
+
+}  // namespace
+
+bool band_plan(const ldpc_code &c, int64_t frames, bool et, BandPlan &p) {
+    if (!c.gallager || !c.regular_col || (c.n & 3)) return false;
+    const int mb = c.n / c.wr;
+    int dev = 0, sms = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const int b0 = std::max(1, (mb + 1023) / 1024);
+    if (b0 > 4) return false;
+    void *k = pick_band_kernel(c.wr, c.wc, b0, et);
+    if (!k) return false;
+    const size_t base = size_t(c.wc) * size_t(c.n) * 4;          // E_hi + L
+    const size_t with_r = base + size_t(c.n) * 4;
+    const size_t reserve = 1024;                                  // static smem + driver
+    if (base + reserve > size_t(optin)) return false;
+    p.r_in_smem = with_r + reserve <= size_t(optin);
+    p.smem = p.r_in_smem ? with_r : base;
+    p.threads = ((mb + b0 - 1) / b0 + 31) / 32 * 32;
+    p.kernel = k;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p.smem)) != cudaSuccess) return false;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p.threads, p.smem) != cudaSuccess || per_sm < 1)
+        return false;
+    p.grid = int(std::max<int64_t>(1, std::min<int64_t>(frames, int64_t(sms) * per_sm)));
+    p.ws_bytes = 256 + (p.r_in_smem ? 0 : size_t(p.grid) * size_t(c.n) * 4);
+    return true;
+}
+
+ldpc_status band_launch(const ldpc_code &c, const BandPlan &p, const float *llr, int64_t frames,
+                        const ldpc_decode_opts &o, uint32_t *bits, uint8_t *syn, int32_t *iters, float *post,
+                        void *ws, size_t ws_bytes, void *stream) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!ws || ws_bytes < p.ws_bytes) return LDPC_ERR_ARG;
+    BandArgs a;
+    a.code = c.dev;
+    a.llr = llr;
+    a.frames = frames;
+    a.max_iter = o.max_iter;
+    a.early_term = o.early_term ? 1 : 0;
+    a.bits = bits;
+    a.syn_ok = syn;
+    a.iters = iters;
+    a.posterior = post;
+    a.frame_counter = static_cast<unsigned long long *>(ws);
+    a.r_global = p.r_in_smem ? nullptr : reinterpret_cast<float *>(static_cast<char *>(ws) + 256);
+    a.r_in_smem = p.r_in_smem ? 1 : 0;
+    if (cudaMemsetAsync(ws, 0, 8, s) != cudaSuccess) return LDPC_ERR_CUDA;
+    void *args[] = {&a};
+    cudaError_t e = cudaLaunchKernel(p.kernel, dim3(unsigned(p.grid)), dim3(unsigned(p.threads)), args, p.smem, s);
+    return e == cudaSuccess ? LDPC_OK : LDPC_ERR_CUDA;
+}
+
+}  // namespace ldpc
