@@ -166,6 +166,21 @@ def run_reference(args):
     return 0
 
 
+def dram_traffic(wl, frames):
+    """DRAM bytes (read + write) per decode launch from the committed ncu
+    --set full capture (profiles/traffic.json), when it was taken on this
+    workload and batch size; else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        e = t.get(wl.name)
+        if e and int(e["frames"]) == int(frames):
+            return float(e["dram_bytes_per_launch"])
+    except Exception:
+        pass
+    return None
+
+
 def workload_config(wl, frames, gpus):
     return {"workload": f"{wl.name}: Gallager ({wl.wc},{wl.wr}) n={wl.n}, {wl.frames} frames in BASELINE.json, "
                         f"{wl.max_iter} {'max (early term.)' if wl.early_term else 'fixed'} SPA iterations, "
@@ -274,7 +289,6 @@ def main():
 
     all_frames = frames * world * args.steps
     value = all_frames * k / (total_ms / 1e3) / 1e9
-    edge_updates = float(ctr[4]) * wl.edges * (args.steps if world == 1 else args.steps)  # executed iterations
     edge_updates_per_step_rank = float(ctr[4]) / world * wl.edges
     dec_avg_s = dec_total_ms / args.steps / 1e3
     achieved = edge_updates_per_step_rank / dec_avg_s / 1e9            # Gedge-updates/s, one GPU
@@ -289,10 +303,11 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = max(1, min(os.cpu_count() or 1, 128))
-        dt, F, kk = cpu_oracle_run(wl, 1, threads)
+        per_thread = max(1, int(os.environ.get("LDPC_CPU_FRAMES_PER_THREAD", "4")))
+        dt, F, kk = cpu_oracle_run(wl, per_thread, threads)
         cpu = {"value": F * kk / dt / 1e9, "unit": "Gbit/s", "cores": threads, "kind": "oracle",
-               "sample": f"{F} frames of {wl.name} ({wl.max_iter} iterations), one per host thread, "
-                         f"{dt:.1f} s wall"}
+               "sample": f"{F} frames of {wl.name} ({wl.max_iter} iterations), {per_thread} per host thread, "
+                         f"{dt:.1f} s wall ({dt * threads:.0f} core-s)"}
 
     if rank == 0:
         line = {
@@ -306,8 +321,9 @@ def main():
             "mean_iterations": iters_mean, "k": k,
             "counters": {"info_bit_errors": int(ctr[0]), "cw_bit_errors": int(ctr[1]),
                          "frame_errors": int(ctr[2]), "undetected": int(ctr[3]), "frames": int(ctr[5])},
-            "roofline": {"bound": "alu", "kernel": "spa_decode_kernel", "achieved": achieved, "peak": peak,
-                         "unit": "Gedge-updates/s", "frac": achieved / peak, "traffic": None,
+            "roofline": {"bound": "alu", "kernel": "ldpc_decode (band_kernel for Gallager codes)",
+                         "achieved": achieved, "peak": peak,
+                         "unit": "Gedge-updates/s", "frac": achieved / peak, "traffic": dram_traffic(wl, frames),
                          "peak_basis": f"SFU: {sms} SMs x 16 MUFU/clk x {clock_mhz:.0f} MHz / 4 MUFU per "
                                        "edge-update (DESIGN.md)"},
             "cpu_baseline": cpu,
