@@ -202,6 +202,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2201_04265_b200 as L
+    from paper_2201_04265_b200 import dist as LD
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -225,7 +226,7 @@ def main():
     info = code.info
     n, k = info.n, info.k
     kw, nw = L.words(k), L.words(n)
-    frame0 = rank * frames       # global frame indices: rank r owns [r F, (r+1) F)
+    frame0, _ = LD.weak_shard(frames, rank)   # global frame indices: rank r owns [r F, (r+1) F)
     d_info = torch.empty((frames, kw), dtype=torch.int32, device=dev)
     d_cw = torch.empty((frames, nw), dtype=torch.int32, device=dev)
     d_llr = torch.empty((frames, n), dtype=torch.float32, device=dev)
@@ -252,7 +253,7 @@ def main():
         d_ctr.zero_()
         L.ldpc_count_errors(code, d_info, d_bits, d_cw, d_syn, d_it, frames, d_ctr)
         if world > 1:
-            dist.all_reduce(d_ctr)
+            LD.all_reduce_counters(d_ctr)
 
     ev_d0 = torch.cuda.Event(enable_timing=True)
     ev_d1 = torch.cuda.Event(enable_timing=True)
@@ -282,7 +283,7 @@ def main():
     total_ms = sum(step_ms)
     t = torch.tensor([total_ms, sum(dec_ms)], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        LD.max_over_ranks(t)
     total_ms, dec_total_ms = float(t[0]), float(t[1])
     ctr = d_ctr.cpu().numpy()
     iters_mean = float(ctr[4]) / max(float(ctr[5]), 1.0)

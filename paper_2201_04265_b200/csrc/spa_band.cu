@@ -61,18 +61,69 @@ __device__ __forceinline__ float psi(float y) {
     const float large = t * h;
     return y > kSplitB ? large : small;
 }
+__device__ __forceinline__ float psi_small(float y) {
+    const float s = y * y;
+    const float q = fmaf(fmaf(fmaf(kQ3, s, kQ2), s, kQ1), s, kQ0);
+    return fmaf(s, q, kC1) - lg2a(y);
+}
+__device__ __forceinline__ float psi_large(float y) {
+    const float t = ex2a(-y);
+    const float u = t * t;
+    return t * fmaf(fmaf(fmaf(kH3, u, kH2), u, kH1), u, kH0);
+}
+
+// psi over a row.  When every input of every active lane of the warp falls in
+// one regime -- the common case once a frame has converged: |L_vc| large
+// (first psi), exclusive sums tiny (second psi) -- only that regime is
+// evaluated (one SFU op and 5 FMA-pipe ops instead of two and 11).
+// LARGE_FIRST orders the two warp votes by the expected regime.  VOTE is off
+// under early termination: a frame stops as soon as it converges, so the
+// uniform regime never lasts and the votes would be pure overhead.
+template <int D, bool LARGE_FIRST, bool VOTE>
+__device__ __forceinline__ void psi_row(const float (&in)[D], float (&out)[D]) {
+    if (!VOTE) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) out[j] = psi(in[j]);
+        return;
+    }
+    const unsigned act = __activemask();
+    float lo = in[0], hi = in[0];
+#pragma unroll
+    for (int j = 1; j < D; ++j) {
+        if (LARGE_FIRST) lo = fminf(lo, in[j]);
+        else hi = fmaxf(hi, in[j]);
+    }
+    if (LARGE_FIRST ? __all_sync(act, lo > kSplitB) : __all_sync(act, hi <= kSplitB)) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) out[j] = LARGE_FIRST ? psi_large(in[j]) : psi_small(in[j]);
+        return;
+    }
+#pragma unroll
+    for (int j = 1; j < D; ++j) {
+        if (LARGE_FIRST) hi = fmaxf(hi, in[j]);
+        else lo = fminf(lo, in[j]);
+    }
+    if (LARGE_FIRST ? __all_sync(act, hi <= kSplitB) : __all_sync(act, lo > kSplitB)) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) out[j] = LARGE_FIRST ? psi_small(in[j]) : psi_large(in[j]);
+        return;
+    }
+#pragma unroll
+    for (int j = 0; j < D; ++j) out[j] = psi(in[j]);
+}
 
 // Check-node update of one row (Eq. 5, readings Q2/Q3/Q7) in log2 units.
 // x[j] = L'_v - E'_cv (not yet clamped); e[j] <- new E'_cv.
-template <int D>
+template <int D, bool VOTE>
 __device__ __forceinline__ void check_row(const float (&x)[D], float (&e)[D]) {
-    float f[D];
+    float f[D], ax[D];
     uint32_t sx = (D & 1) ? 0x80000000u : 0u;     // (-1)^{d_c}
 #pragma unroll
     for (int j = 0; j < D; ++j) {
         sx ^= __float_as_uint(x[j]);
-        f[j] = psi(fminf(fabsf(x[j]), kClampB));
+        ax[j] = fminf(fabsf(x[j]), kClampB);
     }
+    psi_row<D, true, VOTE>(ax, f);
     float ex[D];
     float acc = 0.0f;
 #pragma unroll
@@ -86,9 +137,11 @@ __device__ __forceinline__ void check_row(const float (&x)[D], float (&e)[D]) {
         ex[j] += acc;
         acc += f[j];
     }
+    float g[D];
+    psi_row<D, false, VOTE>(ex, g);
 #pragma unroll
     for (int j = 0; j < D; ++j) {
-        const float mag = fminf(psi(ex[j]), kEMaxB);
+        const float mag = fminf(g[j], kEMaxB);
         const uint32_t sgn = (sx ^ __float_as_uint(x[j])) & 0x80000000u;
         e[j] = __uint_as_float(__float_as_uint(mag) | sgn);
     }
@@ -224,7 +277,7 @@ __global__ void __launch_bounds__(1024, 1) band_kernel(const BandArgs a) {
                         x[j] = lv[j] - e0[k][j];
                         if (ET) synd ^= (lv[j] >= 0.0f) ? 1u : 0u;
                     }
-                    check_row<WR>(x, e0[k]);
+                    check_row<WR, !ET>(x, e0[k]);
                 }
             }
 #pragma unroll
@@ -241,7 +294,7 @@ __global__ void __launch_bounds__(1024, 1) band_kernel(const BandArgs a) {
                         x[j] = lv - e[j];
                         if (ET) synd ^= (lv >= 0.0f) ? 1u : 0u;
                     }
-                    check_row<WR>(x, e);
+                    check_row<WR, !ET>(x, e);
                     sts_row<WR>(smem, uint32_t(r) * WR * 4u, e);
                 }
             }
