@@ -30,78 +30,107 @@ __device__ __forceinline__ U4 philox(U4 c, uint32_t k0, uint32_t k1) {
 }
 
 // ---------------------------------------------------------------------------
-// Encoder, Eq. 3 with G in standard form.  One CTA per tile
-// of FT frames:
-//   1. stage the FT messages (kw words each) in shared memory;
-//   2. parity bit b of frame f = parity(popc(XOR_w m_f[w] & P_b[w])): one warp
-//      per parity column b, lanes stride the kw words (the P column is read
-//      coalesced from L2 once per tile), XOR-accumulate per frame, then one
-//      redux.sync.xor and a popcount per (frame, b) -- 1 LOP3 per 32 GF(2) MACs;
-//   3. the permuted codeword [m | mP] is gathered to H column order with the
-//      inverse permutation and packed by ballot.
-constexpr int kEncFT = 8;
+// Encoder, Eq. 3 with G in standard form: the parity bits
+// are the GF(2) product M P (frames x k times k x (n-k)), bit-packed along k.
+// Kernel 1 (parity) is a register-tiled binary "GEMM" on the INT pipe: a CTA
+// owns 64 frames x 128 parity columns; k is streamed in chunks of 32 words
+// through shared memory (messages as [frame][word], P pre-transposed at bind
+// time as [word][column] so both loads are coalesced); every thread keeps
+// 4 frames x 8 columns of XOR accumulators, acc ^= m & p -- one LOP3 per 32
+// GF(2) multiply-adds -- and the parity of each accumulator is one popc.
+// Parity words are parked in the tail of the frame's output row.  Kernel 2
+// (assemble) scatters [m | m P] to H column order with the inverse
+// permutation, one CTA per frame row, packing 32 bits per ballot.
+constexpr int kEncTF = 64;    // frames per CTA tile
+constexpr int kEncKC = 32;    // message words per k chunk
 
-__global__ void __launch_bounds__(512) encode_kernel(const DeviceCode code, const uint32_t *__restrict__ info,
-                                                     uint32_t *__restrict__ cw, int64_t frames) {
-    extern __shared__ __align__(16) uint32_t esm[];
+__global__ void __launch_bounds__(256) encode_parity_kernel(const DeviceCode code, const uint32_t *__restrict__ info,
+                                                            uint32_t *__restrict__ cw, int64_t frames) {
+    __shared__ uint32_t ms[kEncTF][kEncKC + 1];
+    __shared__ __align__(16) uint32_t ps[kEncKC][kEncColTile];
+    __shared__ uint8_t pbits[kEncTF][kEncColTile / 8];
+    const int kw = code.kw, npp = code.npar_pad, nw = code.nw;
+    const int npw = (code.n - code.k + 31) / 32;
+    const int b0 = blockIdx.x * kEncColTile;
+    const int64_t f0 = int64_t(blockIdx.y) * kEncTF;
+    const int tid = threadIdx.x, tf = tid >> 4, tb = tid & 15;
+    uint32_t acc[4][8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0u;
+
+    for (int w0 = 0; w0 < kw; w0 += kEncKC) {
+        for (int i = tid; i < kEncTF * kEncKC; i += 256) {
+            const int f = i >> 5, w = i & 31;
+            uint32_t x = 0u;
+            if (f0 + f < frames && w0 + w < kw) x = __ldg(info + (f0 + f) * int64_t(kw) + w0 + w);
+            ms[f][w] = x;      // bits beyond k meet zero rows of P: no mask needed
+        }
+        for (int i = tid; i < kEncKC * (kEncColTile / 4); i += 256) {
+            const int w = i >> 5, c4 = i & 31;
+            uint4 x = make_uint4(0u, 0u, 0u, 0u);
+            if (w0 + w < kw) x = __ldg(reinterpret_cast<const uint4 *>(code.pt + size_t(w0 + w) * npp + b0) + c4);
+            *reinterpret_cast<uint4 *>(&ps[w][4 * c4]) = x;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int w = 0; w < kEncKC; ++w) {
+            uint32_t m[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) m[i] = ms[tf * 4 + i][w];
+            const uint4 pa = *reinterpret_cast<const uint4 *>(&ps[w][tb * 8]);
+            const uint4 pb = *reinterpret_cast<const uint4 *>(&ps[w][tb * 8 + 4]);
+            const uint32_t p[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] ^= m[i] & p[j];
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        uint32_t byte = 0u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) byte |= (uint32_t(__popc(acc[i][j])) & 1u) << j;
+        pbits[tf * 4 + i][tb] = uint8_t(byte);
+    }
+    __syncthreads();
+    // parity word q of this tile -> word (b0/32 + q) of the parity area, which
+    // is parked in the last npw words of the frame's output row
+    for (int i = tid; i < kEncTF * (kEncColTile / 32); i += 256) {
+        const int f = i >> 2, q = i & 3;
+        const int pwi = b0 / 32 + q;
+        if (f0 + f < frames && pwi < npw) {
+            const uint8_t *b = &pbits[f][4 * q];
+            const uint32_t word = uint32_t(b[0]) | (uint32_t(b[1]) << 8) | (uint32_t(b[2]) << 16) | (uint32_t(b[3]) << 24);
+            cw[(f0 + f) * int64_t(nw) + (nw - npw) + pwi] = word;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) encode_assemble_kernel(const DeviceCode code, const uint32_t *__restrict__ info,
+                                                              uint32_t *__restrict__ cw, int64_t frames) {
+    extern __shared__ uint32_t asm_buf[];
     const int kw = code.kw, nw = code.nw, k = code.k, n = code.n;
-    const int npar = n - k;
-    const int pw = (n + 31) / 32;              // words of the permuted codeword
-    uint32_t *msg = esm;                       // [FT][kw]
-    uint32_t *cperm = esm + kEncFT * kw;       // [FT][pw]
-    const int64_t f0 = int64_t(blockIdx.x) * kEncFT;
-    const int nf = int(std::min<int64_t>(kEncFT, frames - f0));
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-
-    for (int i = threadIdx.x; i < kEncFT * kw; i += blockDim.x) {
-        const int f = i / kw, w = i - f * kw;
-        uint32_t x = 0;
-        if (f < nf) {
-            x = __ldg(info + (f0 + f) * int64_t(kw) + w);
-            if (w == kw - 1 && (k & 31)) x &= (1u << (k & 31)) - 1u;
-        }
-        msg[i] = x;
-    }
-    for (int i = threadIdx.x; i < kEncFT * pw; i += blockDim.x) cperm[i] = 0;
-    __syncthreads();
-    // systematic part: bits [0, k) of [m | mP] are m
-    for (int i = threadIdx.x; i < kEncFT * kw; i += blockDim.x) {
-        const int f = i / kw, w = i - f * kw;
-        cperm[f * pw + w] = msg[i];
-    }
-    __syncthreads();
-    for (int b = warp; b < npar; b += nwarps) {
-        const uint32_t *col = code.pcols + int64_t(b) * kw;
-        uint32_t acc[kEncFT];
-#pragma unroll
-        for (int f = 0; f < kEncFT; ++f) acc[f] = 0;
-        for (int w = lane; w < kw; w += 32) {
-            const uint32_t p = __ldg(col + w);
-#pragma unroll
-            for (int f = 0; f < kEncFT; ++f) acc[f] ^= msg[f * kw + w] & p;
-        }
-#pragma unroll
-        for (int f = 0; f < kEncFT; ++f) {
-            const uint32_t x = __reduce_xor_sync(0xffffffffu, acc[f]);
-            if (lane == f && (__popc(x) & 1)) {
-                const int pos = k + b;
-                atomicOr(&cperm[f * pw + (pos >> 5)], 1u << (pos & 31));
-            }
-        }
-    }
-    __syncthreads();
-    // scatter to H column order: c[v] = cperm[pinv[v]]
-    for (int f = 0; f < nf; ++f) {
-        uint32_t *out = cw + (f0 + f) * int64_t(nw);
+    const int npw = (n - k + 31) / 32;
+    uint32_t *mrow = asm_buf, *prow = asm_buf + kw;
+    for (int64_t f = blockIdx.x; f < frames; f += gridDim.x) {
+        uint32_t *row = cw + f * int64_t(nw);
+        for (int i = threadIdx.x; i < kw; i += blockDim.x) mrow[i] = __ldg(info + f * int64_t(kw) + i);
+        for (int i = threadIdx.x; i < npw; i += blockDim.x) prow[i] = row[nw - npw + i];
+        __syncthreads();
         for (int v = threadIdx.x; v < nw * 32; v += blockDim.x) {
-            bool bit = false;
+            uint32_t bit = 0u;
             if (v < n) {
                 const int t = __ldg(code.pinv + v);
-                bit = (cperm[f * pw + (t >> 5)] >> (t & 31)) & 1u;
+                bit = t < k ? (mrow[t >> 5] >> (t & 31)) & 1u : (prow[(t - k) >> 5] >> ((t - k) & 31)) & 1u;
             }
-            const uint32_t word = __ballot_sync(0xffffffffu, bit);
-            if (lane == 0) out[v >> 5] = word;
+            const uint32_t word = __ballot_sync(0xffffffffu, bit != 0u);
+            if ((threadIdx.x & 31) == 0) row[v >> 5] = word;
         }
+        __syncthreads();
     }
 }
 
@@ -250,16 +279,21 @@ ldpc_status ldpc_encode(const ldpc_code *code, const uint32_t *d_info, uint32_t 
     if (frames == 0) return LDPC_OK;
     if (!d_info || !d_cw) return LDPC_ERR_ARG;
     const ldpc::DeviceCode &D = code->dev;
-    const int pw = (D.n + 31) / 32;
-    const size_t smem = sizeof(uint32_t) * size_t(ldpc::kEncFT) * size_t(D.kw + pw);
-    if (smem > 200 * 1024) return LDPC_ERR_UNSUPPORTED;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const unsigned col_tiles = unsigned(D.npar_pad / ldpc::kEncColTile);
+    const int64_t max_chunk = int64_t(65535) * ldpc::kEncTF;      // gridDim.y limit
+    for (int64_t f0 = 0; f0 < frames && col_tiles > 0; f0 += max_chunk) {
+        const int64_t nf = std::min<int64_t>(max_chunk, frames - f0);
+        const dim3 grid(col_tiles, unsigned((nf + ldpc::kEncTF - 1) / ldpc::kEncTF));
+        ldpc::encode_parity_kernel<<<grid, 256, 0, s>>>(D, d_info + f0 * D.kw, d_cw + f0 * D.nw, nf);
+    }
+    const size_t smem = sizeof(uint32_t) * size_t(D.kw + (D.n - D.k + 31) / 32);
     if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(ldpc::encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
+        cudaFuncSetAttribute(ldpc::encode_assemble_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
             cudaSuccess)
         return LDPC_ERR_CUDA;
-    const int64_t grid = (frames + ldpc::kEncFT - 1) / ldpc::kEncFT;
-    ldpc::encode_kernel<<<dim3(unsigned(grid)), 512, smem, static_cast<cudaStream_t>(stream)>>>(D, d_info, d_cw,
-                                                                                               frames);
+    const int grid2 = int(std::min<int64_t>(frames, int64_t(ldpc::sm_count()) * 8));
+    ldpc::encode_assemble_kernel<<<grid2, 256, smem, s>>>(D, d_info, d_cw, frames);
     return cudaGetLastError() == cudaSuccess ? LDPC_OK : LDPC_ERR_CUDA;
 }
 

@@ -90,7 +90,8 @@ DeviceLayout compute_layout(const ldpc_code &c, bool with_G) {
         size_t kw = (size_t(c.k) + 31) / 32;
         L.perm = off;  off = align256(off + sizeof(int32_t) * size_t(c.n));
         L.pinv = off;  off = align256(off + sizeof(int32_t) * size_t(c.n));
-        L.pcols = off; off = align256(off + sizeof(uint32_t) * std::max<size_t>(size_t(c.n - c.k) * kw, 1));
+        const size_t npp = (size_t(c.n - c.k) + kEncColTile - 1) / kEncColTile * kEncColTile;
+        L.pt = off;    off = align256(off + sizeof(uint32_t) * std::max<size_t>(kw * npp, 1));
     }
     L.total = off;
     return L;
@@ -331,6 +332,17 @@ ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, vo
         if (nbytes == 0) return true;
         return cudaMemcpyAsync(base + off, src, nbytes, cudaMemcpyHostToDevice, s) == cudaSuccess;
     };
+    // P transposed for the encoder: pt[w][b] = word w of parity column b, columns
+    // padded with zeros to a multiple of kEncColTile.
+    std::vector<uint32_t> pt;
+    auto put_pt = [&](size_t off) -> bool {
+        const size_t kw = (size_t(code->k) + 31) / 32, npar = size_t(code->n - code->k);
+        const size_t npp = (npar + ldpc::kEncColTile - 1) / ldpc::kEncColTile * ldpc::kEncColTile;
+        pt.assign(kw * npp, 0u);
+        for (size_t b = 0; b < npar; ++b)
+            for (size_t w = 0; w < kw; ++w) pt[w * npp + b] = code->pcols[b * kw + w];
+        return put(off, pt.data(), sizeof(uint32_t) * pt.size());
+    };
     bool ok = put(L.row_ptr, code->row_ptr.data(), sizeof(int32_t) * code->row_ptr.size()) &&
               put(L.col_idx, code->col_idx.data(), sizeof(int32_t) * code->col_idx.size()) &&
               put(L.var_ptr, code->var_ptr.data(), sizeof(int32_t) * code->var_ptr.size()) &&
@@ -355,7 +367,7 @@ ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, vo
     if (ok && code->has_G)
         ok = put(L.perm, code->perm.data(), sizeof(int32_t) * code->perm.size()) &&
              put(L.pinv, code->pinv.data(), sizeof(int32_t) * code->pinv.size()) &&
-             put(L.pcols, code->pcols.data(), sizeof(uint32_t) * code->pcols.size());
+             put_pt(L.pt);
     // The host vectors are pageable: cudaMemcpyAsync from pageable memory is
     // staged synchronously, so they may be reused as soon as the call returns.
     if (!ok) return LDPC_ERR_CUDA;
@@ -379,7 +391,8 @@ ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, vo
     D.mb = code->gallager ? code->n / code->wr : 0;
     D.band_lidx = (code->gallager && code->wc >= 2) ? reinterpret_cast<const int32_t *>(base + L.band_lidx) : nullptr;
     D.band_vpos = (code->gallager && code->wc >= 2) ? reinterpret_cast<const int32_t *>(base + L.band_vpos) : nullptr;
-    D.pcols = code->has_G ? reinterpret_cast<const uint32_t *>(base + L.pcols) : nullptr;
+    D.pt = code->has_G ? reinterpret_cast<const uint32_t *>(base + L.pt) : nullptr;
+    D.npar_pad = code->has_G ? (code->n - code->k + ldpc::kEncColTile - 1) / ldpc::kEncColTile * ldpc::kEncColTile : 0;
     return LDPC_OK;
 }
 

@@ -12,6 +12,7 @@
 namespace ldpc {
 
 constexpr int kMaxCheckDegree = 32;   // generic-kernel limit (register arrays)
+constexpr int kEncColTile = 128;      // parity columns per encoder CTA tile
 constexpr float kLlrClamp = 30.0f;    // reading Q7: R and L_vc clamped to +-30
 // reading Q7: |E_cv| <= 2 atanh(1 - 1e-12) = ln(2e12 - 1) = 28.32416830...
 constexpr float kEMax = 28.3241683f;
@@ -24,7 +25,7 @@ struct DeviceLayout {
     size_t var_edges = 0;  // int32 [nnz]       edges of each variable, ascending check
     size_t perm = 0;       // int32 [n]         (after make_G)
     size_t pinv = 0;       // int32 [n]         inverse of perm: position of column v in [m | mP]
-    size_t pcols = 0;      // uint32 [(n-k)*kw] P packed by parity column
+    size_t pt = 0;         // uint32 [kw][npar_pad] P by message word: bit i of [w][b] = P[32w+i][b]
     // Gallager band view (ldpc_make_H codes only), used by the band kernel:
     size_t band_lidx = 0;  // int32 [(wc-1)*n]  edge (band b>=1, position p) -> byte offset of L[pi_b[p]]
     size_t band_vpos = 0;  // int32 [n*(wc-1)]  variable v, band b>=1 -> byte offset of its E in E_hi
@@ -44,7 +45,8 @@ struct DeviceCode {
     const int32_t *var_edges;
     const int32_t *perm;
     const int32_t *pinv;
-    const uint32_t *pcols;
+    const uint32_t *pt;
+    int32_t npar_pad;               // n - k rounded up to kEncColTile
     int32_t gallager, wc, wr, mb;   // band structure (mb = n / wr rows per band)
     const int32_t *band_lidx;
     const int32_t *band_vpos;

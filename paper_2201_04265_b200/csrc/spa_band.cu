@@ -214,6 +214,8 @@ struct BandArgs {
     unsigned long long *frame_counter;   // zeroed before launch
     float *r_global;                     // R' per CTA slot when R does not fit in smem
     int32_t r_in_smem;
+    int32_t row_stride;                  // S = ceil(mb / B0): thread t owns rows t, t+S, ...
+                                         // (balanced: every active thread gets B0 band-0 rows)
 };
 
 __device__ __forceinline__ bool cta_sync_or(bool p) { return __syncthreads_or(p ? 1 : 0) != 0; }
@@ -225,7 +227,7 @@ __global__ void __launch_bounds__(1024, 1) band_kernel(const BandArgs a) {
     __shared__ long long s_frame;
     const DeviceCode &code = a.code;
     const int n = code.n, mb = code.mb;
-    const int T = blockDim.x, tt = threadIdx.x;
+    const int T = blockDim.x, tt = threadIdx.x, S = a.row_stride;
     constexpr int NB = WC - 1;          // bands held in shared memory
     constexpr int B1 = NB * B0;         // max rows of bands >= 1 per thread
     const uint32_t lbase = uint32_t(NB) * uint32_t(n) * 4u;
@@ -268,8 +270,8 @@ __global__ void __launch_bounds__(1024, 1) band_kernel(const BandArgs a) {
             uint32_t synd = 0;
 #pragma unroll
             for (int k = 0; k < B0; ++k) {
-                const int r = tt + k * T;
-                if (r < mb) {
+                const int r = tt + k * S;
+                if (tt < S && r < mb) {
                     float lv[WR], x[WR];
                     lds_row<WR>(smem, lbase + uint32_t(r) * WR * 4u, lv);
 #pragma unroll
@@ -282,8 +284,8 @@ __global__ void __launch_bounds__(1024, 1) band_kernel(const BandArgs a) {
             }
 #pragma unroll
             for (int k = 0; k < B1; ++k) {
-                const int r = tt + k * T;
-                if (r < NB * mb) {
+                const int r = tt + k * S;
+                if (tt < S && r < NB * mb) {
                     int32_t li[WR];
                     float e[WR], x[WR];
                     ldg_idx<WR>(lidx + size_t(r) * WR, li);
@@ -311,8 +313,8 @@ __global__ void __launch_bounds__(1024, 1) band_kernel(const BandArgs a) {
             // ---- a4/a5: variable-node phase, Eq. 7 (owners of band-0 rows)
 #pragma unroll
             for (int k = 0; k < B0; ++k) {
-                const int r = tt + k * T;
-                if (r < mb) {
+                const int r = tt + k * S;
+                if (tt < S && r < mb) {
                     float rv[WR], lv[WR];
                     int32_t vp[WR * NB];
                     lds_row<WR>(reinterpret_cast<const char *>(Rs), uint32_t(r) * WR * 4u, rv);
@@ -435,6 +437,8 @@ ldpc_status band_launch(const ldpc_code &c, const BandPlan &p, const float *llr,
     a.frame_counter = static_cast<unsigned long long *>(ws);
     a.r_global = p.r_in_smem ? nullptr : reinterpret_cast<float *>(static_cast<char *>(ws) + 256);
     a.r_in_smem = p.r_in_smem ? 1 : 0;
+    const int b0 = (c.n / c.wr + 1023) / 1024;
+    a.row_stride = (c.n / c.wr + b0 - 1) / b0;
     if (cudaMemsetAsync(ws, 0, 8, s) != cudaSuccess) return LDPC_ERR_CUDA;
     void *args[] = {&a};
     cudaError_t e = cudaLaunchKernel(p.kernel, dim3(unsigned(p.grid)), dim3(unsigned(p.threads)), args, p.smem, s);
