@@ -47,10 +47,67 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C4", choices=sorted(W.ALL))
     ap.add_argument("--frames", type=int, default=0, help="override frames per GPU per step")
-    ap.add_argument("--e2e-frames", type=int, default=65536)
+    ap.add_argument("--e2e-frames", type=int, default=0, help="cap on e2e frames per step (0 = the batch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--mode", choices=["batch", "stream"], default="batch",
+                    help="stream = frames decoded one per ldpc_decode call, serially (the paper's stream mode)")
     return ap.parse_args()
+
+
+def run_stream(args):
+    """Stream mode (batch 1): one frame per ldpc_decode call, issued
+    serially on one stream; the serial calls are captured once in a CUDA graph
+    and replayed, so the number is per-frame device latency, not launch cost."""
+    import torch
+
+    import paper_2201_04265_b200 as L
+    torch.cuda.set_device(0)
+    wl = W.ALL[args.config]
+    code = L.ldpc_code_bind_device(L.ldpc_make_G(L.ldpc_make_H(wl.n, wl.wc, wl.wr, W.CODE_SEED)))
+    k, n = code.info.k, code.info.n
+    G = 64
+    info = torch.empty((G, L.words(k)), dtype=torch.int32, device="cuda")
+    cw = torch.empty((G, L.words(n)), dtype=torch.int32, device="cuda")
+    llr = torch.empty((G, n), dtype=torch.float32, device="cuda")
+    L.ldpc_gen_info(wl.frame_seeds[0], 0, G, k, info)
+    L.ldpc_encode(code, info, cw, G)
+    L.ldpc_channel(code, wl.frame_seeds[0], 0, G, cw, wl.sigma(), llr)
+    bits = torch.empty((G, L.words(n)), dtype=torch.int32, device="cuda")
+    syn = torch.empty(G, dtype=torch.uint8, device="cuda")
+    it = torch.empty(G, dtype=torch.int32, device="cuda")
+    wsb = max(L.ldpc_decode_workspace_bytes(code, 1, wl.max_iter, wl.early_term), 256)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+
+    def serial():
+        for f in range(G):
+            L.ldpc_decode(code, llr[f:f + 1], 1, bits[f:f + 1], syn[f:f + 1], it[f:f + 1], None, ws,
+                          wl.max_iter, wl.early_term, stream=s)
+
+    with torch.cuda.stream(s):
+        serial()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        serial()
+    for _ in range(args.warmup):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(args.steps):
+        g.replay()
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / (args.steps * G)
+    iters = float(it.double().mean())
+    print(json.dumps({"mode": "stream", "metric": "stream-mode decode latency per frame", "value": ms * 1e3,
+                      "unit": "us", "frames_per_s": 1e3 / ms, "info_gbit_s": k / (ms * 1e-3) / 1e9,
+                      "edge_updates_per_s": wl.edges * iters / (ms * 1e-3), "mean_iterations": iters,
+                      "config": workload_config(wl, 1, 1), "frames_timed": args.steps * G,
+                      "note": "one CTA decodes the frame; serial calls replayed from a CUDA graph"}), flush=True)
+    return 0
 
 
 def measured_peaks():
@@ -196,6 +253,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.mode == "stream":
+        return run_stream(args)
 
     import numpy as np
     import torch
@@ -344,7 +403,11 @@ def e2e_measure(L, code, wl, args, dev, frame0, k, n, kw, nw, world):
     step's info bits and LLRs, encode, decode, count, D2H of the decoded bits
     and the counters, all inside the timed region."""
     import torch
-    F = min(args.e2e_frames, args.frames or wl.frames)
+    F = args.frames or wl.frames
+    if args.e2e_frames:
+        F = min(F, args.e2e_frames)
+    Fc = min(F, 16384)                       # pipeline chunk
+    nchunks = (F + Fc - 1) // Fc
     try:
         h_info = torch.empty((F, kw), dtype=torch.int32, pin_memory=True)
         h_llr = torch.empty((F, n), dtype=torch.float32, pin_memory=True)
@@ -352,48 +415,77 @@ def e2e_measure(L, code, wl, args, dev, frame0, k, n, kw, nw, world):
         h_ctr = torch.empty(6, dtype=torch.int64, pin_memory=True)
     except Exception as e:  # pragma: no cover
         return {"value": None, "unit": "Gbit/s", "error": f"pinned alloc failed: {e}"}
-    # fill the host inputs with the workload's frames (generated once, untimed)
-    d_info = torch.empty((F, kw), dtype=torch.int32, device=dev)
-    d_cw = torch.empty((F, nw), dtype=torch.int32, device=dev)
-    d_llr = torch.empty((F, n), dtype=torch.float32, device=dev)
+    bufs = [dict(info=torch.empty((Fc, kw), dtype=torch.int32, device=dev),
+                 cw=torch.empty((Fc, nw), dtype=torch.int32, device=dev),
+                 llr=torch.empty((Fc, n), dtype=torch.float32, device=dev),
+                 bits=torch.empty((Fc, nw), dtype=torch.int32, device=dev),
+                 syn=torch.empty(Fc, dtype=torch.uint8, device=dev),
+                 it=torch.empty(Fc, dtype=torch.int32, device=dev)) for _ in range(2)]
+    # the workload's frames, generated once on the device and parked in host memory (untimed)
     seed = wl.frame_seeds[0]
-    L.ldpc_gen_info(seed, frame0, F, k, d_info)
-    L.ldpc_encode(code, d_info, d_cw, F)
-    L.ldpc_channel(code, seed, frame0, F, d_cw, wl.sigma(), d_llr)
-    h_info.copy_(d_info)
-    h_llr.copy_(d_llr)
-    d_bits = torch.empty((F, nw), dtype=torch.int32, device=dev)
-    d_syn = torch.empty(F, dtype=torch.uint8, device=dev)
-    d_it = torch.empty(F, dtype=torch.int32, device=dev)
+    for c in range(nchunks):
+        a, m = c * Fc, min(Fc, F - c * Fc)
+        b = bufs[0]
+        L.ldpc_gen_info(seed, frame0 + a, m, k, b["info"])
+        L.ldpc_encode(code, b["info"], b["cw"], m)
+        L.ldpc_channel(code, seed, frame0 + a, m, b["cw"], wl.sigma(), b["llr"])
+        h_info[a:a + m].copy_(b["info"][:m])
+        h_llr[a:a + m].copy_(b["llr"][:m])
     d_ctr = torch.zeros(6, dtype=torch.int64, device=dev)
-    wsb = L.ldpc_decode_workspace_bytes(code, F, wl.max_iter, wl.early_term, args.variant)
+    wsb = L.ldpc_decode_workspace_bytes(code, Fc, wl.max_iter, wl.early_term, args.variant)
     d_ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev) if wsb else None
+    s_in, s_cmp, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_cmp = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(2)]
 
     def step():
-        d_info.copy_(h_info, non_blocking=True)
-        d_llr.copy_(h_llr, non_blocking=True)
-        L.ldpc_encode(code, d_info, d_cw, F)
-        L.ldpc_decode(code, d_llr, F, d_bits, d_syn, d_it, None, d_ws, wl.max_iter, wl.early_term, args.variant)
-        d_ctr.zero_()
-        L.ldpc_count_errors(code, d_info, d_bits, d_cw, d_syn, d_it, F, d_ctr)
-        h_bits.copy_(d_bits, non_blocking=True)
-        h_ctr.copy_(d_ctr, non_blocking=True)
+        """Three-stage pipeline over chunks: H2D (s_in) -> encode, decode,
+        count (s_cmp) -> D2H of the decoded bits (s_out), double-buffered."""
+        with torch.cuda.stream(s_cmp):
+            d_ctr.zero_()
+        for c in range(nchunks):
+            a, m, i = c * Fc, min(Fc, F - c * Fc), c % 2
+            b = bufs[i]
+            if c >= 2:
+                s_in.wait_event(ev_cmp[i])          # buffer i's inputs consumed
+            with torch.cuda.stream(s_in):
+                b["info"][:m].copy_(h_info[a:a + m], non_blocking=True)
+                b["llr"][:m].copy_(h_llr[a:a + m], non_blocking=True)
+                ev_in[i].record(s_in)
+            s_cmp.wait_event(ev_in[i])
+            if c >= 2:
+                s_cmp.wait_event(ev_out[i])         # buffer i's bits drained
+            L.ldpc_encode(code, b["info"], b["cw"], m, stream=s_cmp)
+            L.ldpc_decode(code, b["llr"], m, b["bits"], b["syn"], b["it"], None, d_ws, wl.max_iter,
+                          wl.early_term, args.variant, stream=s_cmp)
+            L.ldpc_count_errors(code, b["info"], b["bits"], b["cw"], b["syn"], b["it"], m, d_ctr, stream=s_cmp)
+            ev_cmp[i].record(s_cmp)
+            s_out.wait_event(ev_cmp[i])
+            with torch.cuda.stream(s_out):
+                h_bits[a:a + m].copy_(b["bits"][:m], non_blocking=True)
+                ev_out[i].record(s_out)
+        with torch.cuda.stream(s_out):
+            h_ctr.copy_(d_ctr, non_blocking=True)
 
     step()
     torch.cuda.synchronize()
     steps = max(1, args.steps)
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(s_in)
     for _ in range(steps):
+        s_in.wait_stream(s_out)                     # steps do not overlap each other
         step()
-    e.record()
+    s_in.wait_stream(s_out)
+    end.record(s_in)
     torch.cuda.synchronize()
-    ms = s.elapsed_time(e)
+    ms = start.elapsed_time(end)
     bi = F * kw * 4 + F * n * 4
     bo = F * nw * 4 + 6 * 8
     return {"value": world * steps * F * k / (ms / 1e3) / 1e9, "unit": "Gbit/s", "h2d_bytes_per_step": bi,
             "d2h_bytes_per_step": bo, "frames_per_gpu_per_step": F,
-            "note": "pinned host buffers; copies serialised with compute on one stream"}
+            "note": f"pinned host buffers; H2D / encode+decode+count / D2H pipelined over {nchunks} chunks of "
+                    f"{Fc} frames on three streams"}
 
 
 if __name__ == "__main__":
