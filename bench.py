@@ -91,14 +91,18 @@ def run_stream(args):
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=s):
         serial()
-    for _ in range(args.warmup):
-        g.replay()
+    it.zero_()
+    with torch.cuda.stream(s):              # graph replays on the current stream
+        for _ in range(args.warmup):
+            g.replay()
     torch.cuda.synchronize()
+    assert int(it.min()) >= 1, "graph replay did not decode"
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(s)
-    for _ in range(args.steps):
-        g.replay()
-    e1.record(s)
+    with torch.cuda.stream(s):
+        e0.record(s)
+        for _ in range(args.steps):
+            g.replay()
+        e1.record(s)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / (args.steps * G)
     iters = float(it.double().mean())

@@ -77,6 +77,44 @@ void run(int sms, float *d_out, unsigned long long *d_cyc, int remote_shift, con
            double(threads) * iters * 8 / mean);
 }
 
+// Random 4-byte gathers from an L2-resident global buffer (words = 2^log2w).
+__global__ void l2_gather(const float *__restrict__ buf, int log2w, int iters, float *out,
+                          unsigned long long *cycles) {
+    uint32_t s = threadIdx.x * 2654435761u + blockIdx.x * 40503u + 12345u;
+    float acc = 0.f;
+    unsigned long long t0 = clock64();
+    for (int i = 0; i < iters; ++i) {
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            s = s * 1664525u + 1013904223u;
+            v[q] = __ldcg(buf + (s >> (32 - log2w)));
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc += v[q];
+    }
+    unsigned long long t1 = clock64();
+    out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+    if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+}
+
+void run_l2(int sms, float *d_out, unsigned long long *d_cyc, int log2w) {
+    float *buf;
+    cudaMalloc(&buf, sizeof(float) << log2w);
+    cudaMemset(buf, 0, sizeof(float) << log2w);
+    const int threads = 1024, iters = 128;
+    for (int rep = 0; rep < 2; ++rep) l2_gather<<<sms, threads>>>(buf, log2w, iters, d_out, d_cyc);
+    cudaDeviceSynchronize();
+    std::vector<unsigned long long> cyc(sms);
+    cudaMemcpy(cyc.data(), d_cyc, sizeof(unsigned long long) * sms, cudaMemcpyDeviceToHost);
+    double mean = 0;
+    for (auto c : cyc) mean += double(c);
+    mean /= sms;
+    printf("global random gather, %6.1f MB buffer: %.2f loads/clk/SM\n", (4.0 * (1 << log2w)) / 1e6,
+           double(threads) * iters * 8 / mean);
+    cudaFree(buf);
+}
+
 int main() {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -92,5 +130,6 @@ int main() {
     run<2, true>(sms, d_out, d_cyc, 3, "uniform rank (1/2 rem)");
     run<4, true>(sms, d_out, d_cyc, 3, "uniform rank (3/4 rem)");
     run<8, true>(sms, d_out, d_cyc, 3, "uniform rank (7/8 rem)");
+    for (int lw : {18, 22, 24, 25}) run_l2(sms, d_out, d_cyc, lw);
     return 0;
 }
