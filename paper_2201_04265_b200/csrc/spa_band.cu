@@ -36,6 +36,8 @@ constexpr float kEMaxB = 40.86313714f;    // log2(2e12 - 1) = E_MAX log2(e)
 //   y <= 1.8033688: psi = C1 - lg2(y) + y^2 q(y^2)     (one lg2)
 //   y >  1.8033688: psi = t h(t^2),  t = 2^-y          (one ex2)
 constexpr float kSplitB = 1.8033688f;
+constexpr float kUltraLargeB = 10.0f;           // psi(y) = h0 2^-y within 3.2e-7 relative
+constexpr float kUltraSmallB = 0.0009765625f;   // psi(y) = C1 - lg2(y) within 5e-9 relative
 constexpr float kC1 = 1.528766373f;
 constexpr float kQ0 = 0.0577617388f, kQ1 = -0.00161740689f, kQ2 = 5.33304814e-05f, kQ3 = -1.50169545e-06f;
 constexpr float kH0 = 2.88539008f, kH1 = 0.961820197f, kH2 = 0.574983425f, kH3 = 0.461572595f;
@@ -92,6 +94,14 @@ __device__ __forceinline__ void psi_row(const float (&in)[D], float (&out)[D]) {
     for (int j = 1; j < D; ++j) {
         if (LARGE_FIRST) lo = fminf(lo, in[j]);
         else hi = fmaxf(hi, in[j]);
+    }
+    // Deep-converged tiers: y >= 10 -> psi = h0 2^-y (dropped terms <= 3.2e-7
+    // relative); y <= 2^-10 -> psi = C1 - lg2 y (dropped term <= 5.5e-8 against
+    // psi >= 11.5).  One SFU op and one FMA-pipe op per input.
+    if (LARGE_FIRST ? __all_sync(act, lo >= kUltraLargeB) : __all_sync(act, hi <= kUltraSmallB)) {
+#pragma unroll
+        for (int j = 0; j < D; ++j) out[j] = LARGE_FIRST ? kH0 * ex2a(-in[j]) : kC1 - lg2a(in[j]);
+        return;
     }
     if (LARGE_FIRST ? __all_sync(act, lo > kSplitB) : __all_sync(act, hi <= kSplitB)) {
 #pragma unroll
