@@ -145,8 +145,10 @@ ldpc_status ldpc_decode_workspace_bytes(const ldpc_code *code, int64_t frames,
  * Check update E_cv = (-1)^{d_c} prod sgn(L_v'c) * phi(sum phi(|L_v'c|)),
  * phi(x) = -ln tanh(x/2) (Eq. 5, reading Q2/Q3), L_v'c clamped to
  * +-30, |E_cv| <= E_MAX = 2 atanh(1 - 1e-12) (reading Q7).
- * opts->variant: 0 auto, 1 on-chip team-per-frame, 2 global-state
- * CTA-per-frame. */
+ * opts->variant: 0 auto; 1 generic on-chip (team per frame); 2 generic
+ * global-state (CTA per frame, any n); 3 Gallager band kernel, check-major E;
+ * 4 Gallager band kernel, variable-major E (3 and 4 need an ldpc_make_H code
+ * whose frame fits one SM; LDPC_ERR_UNSUPPORTED otherwise). */
 ldpc_status ldpc_decode(const ldpc_code *code, const float *d_llr, int64_t frames,
                         const ldpc_decode_opts *opts, uint32_t *d_bits,
                         uint8_t *d_syndrome_ok, int32_t *d_iters, float *d_posterior,

@@ -53,3 +53,13 @@ C4 = Workload("C4", 16200, 3, 6, 200000, 50, False, (1.5,), (401,), "with bit-pa
 C5 = Workload("C5", 64800, 3, 6, 1000000, 50, False, (1.2,), (501,), "sharded over 1/2/4/8 GPUs")
 
 ALL = {w.name: w for w in (C1, C2, C3_R14, C3_R12, C3_R34, C4, C5)}
+
+# The paper's own experiment, Table I: n = 1032, 12 ones per row,
+# 9/6/3 per column (design rates 1/4, 1/2, 3/4), 10 decoding iterations, 1000
+# vectors.  The paper states no SNR; Eb/N0 = 2.5 dB (as C3) is this build's
+# choice.
+T1_R14 = Workload("T1-R1/4", 1032, 9, 12, 1000, 10, False, (2.5,), (601,), "Table I, wc = 9")
+T1_R12 = Workload("T1-R1/2", 1032, 6, 12, 1000, 10, False, (2.5,), (602,), "Table I, wc = 6")
+T1_R34 = Workload("T1-R3/4", 1032, 3, 12, 1000, 10, False, (2.5,), (603,), "Table I, wc = 3")
+TABLE_I = {w.name: w for w in (T1_R14, T1_R12, T1_R34)}
+ALL.update(TABLE_I)

@@ -108,7 +108,7 @@ const char *ldpc_status_str(ldpc_status s) {
         case LDPC_ERR_NO_INFO_BITS: return "code has no information bits (k == 0)";
         case LDPC_ERR_DIM: return "dimension mismatch";
         case LDPC_ERR_STATE: return "call out of order (make_G / bind_device missing)";
-        case LDPC_ERR_UNSUPPORTED: return "unsupported code (degree > 32?)";
+        case LDPC_ERR_UNSUPPORTED: return "unsupported code or decoder variant for this code";
         case LDPC_ERR_CUDA: return "CUDA runtime error";
         case LDPC_ERR_NOMEM: return "out of host memory";
     }

@@ -89,11 +89,13 @@ struct BandPlan {
     int grid = 0;
     size_t smem = 0;
     bool r_in_smem = false;
+    bool vm = false;            // E of bands >= 1 stored variable-major
     size_t ws_bytes = 0;
 };
 // false when the code is not eligible (not from ldpc_make_H, unsupported
 // (wc, wr), n % 4 != 0, or the frame does not fit one SM's shared memory).
-bool band_plan(const ldpc_code &c, int64_t frames, bool et, BandPlan &p);
+// variant: 0 auto, 3 check-major E, 4 variable-major E.
+bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPlan &p);
 ldpc_status band_launch(const ldpc_code &c, const BandPlan &p, const float *llr, int64_t frames,
                         const ldpc_decode_opts &o, uint32_t *bits, uint8_t *syn, int32_t *iters, float *post,
                         void *ws, size_t ws_bytes, void *stream);

@@ -231,8 +231,10 @@ struct BandArgs {
 __device__ __forceinline__ bool cta_sync_or(bool p) { return __syncthreads_or(p ? 1 : 0) != 0; }
 
 // WR: row weight, WC: column weight (bands), B0: max band-0 rows per thread.
-template <int WR, int WC, int B0, bool ET>
-__global__ void __launch_bounds__(1024, 1) band_kernel(const BandArgs a) {
+// wc > 3 (Table I codes, n = 1032) use small CTAs: the 256-thread bound leaves
+// room for the wider per-row state.
+template <int WR, int WC, int B0, bool ET, bool VM>
+__global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const BandArgs a) {
     extern __shared__ __align__(16) char smem[];
     __shared__ long long s_frame;
     const DeviceCode &code = a.code;
@@ -299,7 +301,14 @@ __global__ void __launch_bounds__(1024, 1) band_kernel(const BandArgs a) {
                     int32_t li[WR];
                     float e[WR], x[WR];
                     ldg_idx<WR>(lidx + size_t(r) * WR, li);
-                    lds_row<WR>(smem, uint32_t(r) * WR * 4u, e);
+                    // VM: E_b is variable-major, at the variable's L offset + delta_b
+                    const int32_t delta = VM ? int32_t((r / mb) * n * 4) - int32_t(lbase) : 0;
+                    if (VM) {
+#pragma unroll
+                        for (int j = 0; j < WR; ++j) e[j] = *reinterpret_cast<const float *>(smem + li[j] + delta);
+                    } else {
+                        lds_row<WR>(smem, uint32_t(r) * WR * 4u, e);
+                    }
 #pragma unroll
                     for (int j = 0; j < WR; ++j) {
                         const float lv = *reinterpret_cast<const float *>(smem + li[j]);
@@ -307,7 +316,12 @@ __global__ void __launch_bounds__(1024, 1) band_kernel(const BandArgs a) {
                         if (ET) synd ^= (lv >= 0.0f) ? 1u : 0u;
                     }
                     check_row<WR, !ET>(x, e);
-                    sts_row<WR>(smem, uint32_t(r) * WR * 4u, e);
+                    if (VM) {
+#pragma unroll
+                        for (int j = 0; j < WR; ++j) *reinterpret_cast<float *>(smem + li[j] + delta) = e[j];
+                    } else {
+                        sts_row<WR>(smem, uint32_t(r) * WR * 4u, e);
+                    }
                 }
             }
             if (ET) {
@@ -326,15 +340,28 @@ __global__ void __launch_bounds__(1024, 1) band_kernel(const BandArgs a) {
                 const int r = tt + k * S;
                 if (tt < S && r < mb) {
                     float rv[WR], lv[WR];
-                    int32_t vp[WR * NB];
                     lds_row<WR>(reinterpret_cast<const char *>(Rs), uint32_t(r) * WR * 4u, rv);
-                    ldg_idx<WR * NB>(vpos + size_t(r) * WR * NB, vp);
+                    if (VM) {
+                        // this row's variables are contiguous in every band's E_b
 #pragma unroll
-                    for (int j = 0; j < WR; ++j) {
-                        float s = rv[j] + e0[k][j];
+                        for (int j = 0; j < WR; ++j) lv[j] = rv[j] + e0[k][j];
 #pragma unroll
-                        for (int b = 0; b < NB; ++b) s += *reinterpret_cast<const float *>(smem + vp[j * NB + b]);
-                        lv[j] = s;
+                        for (int b = 0; b < NB; ++b) {
+                            float eb[WR];
+                            lds_row<WR>(smem, uint32_t(b) * n * 4u + uint32_t(r) * WR * 4u, eb);
+#pragma unroll
+                            for (int j = 0; j < WR; ++j) lv[j] += eb[j];
+                        }
+                    } else {
+                        int32_t vp[WR * NB];
+                        ldg_idx<WR * NB>(vpos + size_t(r) * WR * NB, vp);
+#pragma unroll
+                        for (int j = 0; j < WR; ++j) {
+                            float s = rv[j] + e0[k][j];
+#pragma unroll
+                            for (int b = 0; b < NB; ++b) s += *reinterpret_cast<const float *>(smem + vp[j * NB + b]);
+                            lv[j] = s;
+                        }
                     }
                     sts_row<WR>(smem, lbase + uint32_t(r) * WR * 4u, lv);
                 }
@@ -373,35 +400,54 @@ __global__ void __launch_bounds__(1024, 1) band_kernel(const BandArgs a) {
 }
 
 template <int WR, int WC, int B0>
-void *pick_et(bool et) {
-    return et ? reinterpret_cast<void *>(&band_kernel<WR, WC, B0, true>)
-              : reinterpret_cast<void *>(&band_kernel<WR, WC, B0, false>);
+void *pick_et(bool et, bool vm) {
+    if (vm)
+        return et ? reinterpret_cast<void *>(&band_kernel<WR, WC, B0, true, true>)
+                  : reinterpret_cast<void *>(&band_kernel<WR, WC, B0, false, true>);
+    return et ? reinterpret_cast<void *>(&band_kernel<WR, WC, B0, true, false>)
+              : reinterpret_cast<void *>(&band_kernel<WR, WC, B0, false, false>);
 }
 
 template <int WR, int WC>
-void *pick_b0(int b0, bool et) {
+void *pick_b0(int b0, bool et, bool vm) {
     switch (b0) {
-        case 1: return pick_et<WR, WC, 1>(et);
-        case 2: return pick_et<WR, WC, 2>(et);
-        case 3: return pick_et<WR, WC, 3>(et);
-        case 4: return pick_et<WR, WC, 4>(et);
+        case 1: return pick_et<WR, WC, 1>(et, vm);
+        case 2: return pick_et<WR, WC, 2>(et, vm);
+        case 3: return pick_et<WR, WC, 3>(et, vm);
+        case 4: return pick_et<WR, WC, 4>(et, vm);
     }
     return nullptr;
 }
 
-void *pick_band_kernel(int wr, int wc, int b0, bool et) {
-    if (wc != 3) return nullptr;
-    switch (wr) {
-        case 4: return pick_b0<4, 3>(b0, et);
-        case 6: return pick_b0<6, 3>(b0, et);
-        case 12: return pick_b0<12, 3>(b0, et);
+template <int WR, int WC>
+void *pick_b0_small(int b0, bool et, bool vm) {
+    switch (b0) {
+        case 1: return pick_et<WR, WC, 1>(et, vm);
+        case 2: return pick_et<WR, WC, 2>(et, vm);
+    }
+    return nullptr;
+}
+
+// (wc, wr) instantiated: the BASELINE.json configs ((3, 4), (3, 6), (3, 12))
+// and the paper's Table I (wr = 12 with wc = 9, 6, 3).
+void *pick_band_kernel(int wr, int wc, int b0, bool et, bool vm) {
+    if (wc == 3) {
+        switch (wr) {
+            case 4: return pick_b0<4, 3>(b0, et, vm);
+            case 6: return pick_b0<6, 3>(b0, et, vm);
+            case 12: return pick_b0<12, 3>(b0, et, vm);
+        }
+    } else if (wr == 12 && wc == 6) {
+        return pick_b0_small<12, 6>(b0, et, vm);
+    } else if (wr == 12 && wc == 9) {
+        return pick_b0_small<12, 9>(b0, et, vm);
     }
     return nullptr;
 }
 
 }  // namespace
 
-bool band_plan(const ldpc_code &c, int64_t frames, bool et, BandPlan &p) {
+bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPlan &p) {
     if (!c.gallager || !c.regular_col || (c.n & 3)) return false;
     const int mb = c.n / c.wr;
     int dev = 0, sms = 0, optin = 0;
@@ -410,13 +456,19 @@ bool band_plan(const ldpc_code &c, int64_t frames, bool et, BandPlan &p) {
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     const int b0 = std::max(1, (mb + 1023) / 1024);
     if (b0 > 4) return false;
-    void *k = pick_band_kernel(c.wr, c.wc, b0, et);
-    if (!k) return false;
     const size_t base = size_t(c.wc) * size_t(c.n) * 4;          // E_hi + L
     const size_t with_r = base + size_t(c.n) * 4;
     const size_t reserve = 1024;                                  // static smem + driver
     if (base + reserve > size_t(optin)) return false;
     p.r_in_smem = with_r + reserve <= size_t(optin);
+    // Variable-major E (variant 4) drops the variable phase's index loads and
+    // gathers; it pays off when the indices no longer fit in L1 (large n).
+    p.vm = variant == 4 || (variant == 0 && (!p.r_in_smem || c.wc > 3));
+    void *k = pick_band_kernel(c.wr, c.wc, b0, et, p.vm);
+    if (!k) return false;
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) return false;
+    if (((mb + b0 - 1) / b0 + 31) / 32 * 32 > fa.maxThreadsPerBlock) return false;
     p.smem = p.r_in_smem ? with_r : base;
     p.threads = ((mb + b0 - 1) / b0 + 31) / 32 * 32;
     p.kernel = k;
