@@ -85,6 +85,10 @@ DeviceLayout compute_layout(const ldpc_code &c, bool with_G) {
         const size_t nb = size_t(c.wc - 1) * size_t(c.n);
         L.band_lidx = off; off = align256(off + sizeof(int32_t) * nb);
         L.band_vpos = off; off = align256(off + sizeof(int32_t) * nb);
+        if (band_cluster_size(c.n, c.wc, c.wr) > 0) {
+            L.cband_lidx = off; off = align256(off + sizeof(int32_t) * nb);
+            L.cband_vpos = off; off = align256(off + sizeof(int32_t) * nb);
+        }
     }
     if (with_G) {
         size_t kw = (size_t(c.k) + 31) / 32;
@@ -363,6 +367,26 @@ ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, vo
             }
         ok = put(L.band_lidx, lidx.data(), sizeof(int32_t) * lidx.size()) &&
              put(L.band_vpos, vpos.data(), sizeof(int32_t) * vpos.size());
+        const int C = ldpc::band_cluster_size(n, wc, code->wr);
+        if (ok && C > 0) {
+            // CTA q of a cluster owns band rows [q mbq, (q+1) mbq) of every band and
+            // the variables [q nq, (q+1) nq) of its band-0 rows.  Its shared image:
+            // E_hi [(b-1)][local row][j] then L [local variable].
+            const int32_t wr = code->wr, mb = n / wr, mbq = mb / C, nq = n / C;
+            const int32_t lbase_c = (wc - 1) * mbq * wr * 4;
+            for (int32_t b = 1; b < wc; ++b)
+                for (int32_t p = 0; p < n; ++p) {
+                    const int32_t v = code->col_idx[size_t(b) * n + p];
+                    const int32_t row_owner = (p / wr) / mbq, var_owner = v / nq;
+                    lidx[size_t(b - 1) * n + p] =
+                        row_owner == var_owner ? lbase_c + 4 * (v - var_owner * nq) : ~v;
+                    const int32_t e_local = 4 * ((b - 1) * mbq * wr + (p - row_owner * mbq * wr));
+                    vpos[size_t(v) * (wc - 1) + (b - 1)] =
+                        row_owner == var_owner ? e_local : ~int32_t((b - 1) * n + p);
+                }
+            ok = put(L.cband_lidx, lidx.data(), sizeof(int32_t) * lidx.size()) &&
+                 put(L.cband_vpos, vpos.data(), sizeof(int32_t) * vpos.size());
+        }
     }
     if (ok && code->has_G)
         ok = put(L.perm, code->perm.data(), sizeof(int32_t) * code->perm.size()) &&
@@ -391,6 +415,9 @@ ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, vo
     D.mb = code->gallager ? code->n / code->wr : 0;
     D.band_lidx = (code->gallager && code->wc >= 2) ? reinterpret_cast<const int32_t *>(base + L.band_lidx) : nullptr;
     D.band_vpos = (code->gallager && code->wc >= 2) ? reinterpret_cast<const int32_t *>(base + L.band_vpos) : nullptr;
+    D.cluster = (code->gallager && code->wc >= 2) ? ldpc::band_cluster_size(code->n, code->wc, code->wr) : 0;
+    D.cband_lidx = D.cluster ? reinterpret_cast<const int32_t *>(base + L.cband_lidx) : nullptr;
+    D.cband_vpos = D.cluster ? reinterpret_cast<const int32_t *>(base + L.cband_vpos) : nullptr;
     D.pt = code->has_G ? reinterpret_cast<const uint32_t *>(base + L.pt) : nullptr;
     D.npar_pad = code->has_G ? (code->n - code->k + ldpc::kEncColTile - 1) / ldpc::kEncColTile * ldpc::kEncColTile : 0;
     return LDPC_OK;

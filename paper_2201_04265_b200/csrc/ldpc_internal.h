@@ -29,6 +29,11 @@ struct DeviceLayout {
     // Gallager band view (ldpc_make_H codes only), used by the band kernel:
     size_t band_lidx = 0;  // int32 [(wc-1)*n]  edge (band b>=1, position p) -> byte offset of L[pi_b[p]]
     size_t band_vpos = 0;  // int32 [n*(wc-1)]  variable v, band b>=1 -> byte offset of its E in E_hi
+    // Cluster band view (frames too large for one SM: C CTAs share a frame):
+    // value >= 0: byte offset in the owning CTA's shared memory; value < 0:
+    // ~(element index) into the frame's global copy (Lg for lidx, Eg for vpos).
+    size_t cband_lidx = 0; // int32 [(wc-1)*n]
+    size_t cband_vpos = 0; // int32 [n*(wc-1)]
     size_t total = 0;
 };
 
@@ -50,7 +55,21 @@ struct DeviceCode {
     int32_t gallager, wc, wr, mb;   // band structure (mb = n / wr rows per band)
     const int32_t *band_lidx;
     const int32_t *band_vpos;
+    int32_t cluster;                // C of the cluster band view (0: none)
+    const int32_t *cband_lidx;
+    const int32_t *cband_vpos;
 };
+
+// Cluster size for the cluster band kernel: the smallest power of two C <= 16
+// with mb % C == 0 whose per-CTA share (E of bands >= 1 + L) fits 200 KB; 0
+// when a frame fits one SM (or no such C exists).
+inline int band_cluster_size(int32_t n, int32_t wc, int32_t wr) {
+    const size_t one = size_t(wc) * size_t(n) * 4;
+    if (one + 1024 <= 227 * 1024) return 0;
+    for (int C = 2; C <= 16; C *= 2)
+        if ((n / wr) % C == 0 && one / C <= 200 * 1024) return C;
+    return 0;
+}
 
 // Shared-memory image of one frame in the band kernel (floats):
 //   E_hi[(wc-1) n] (bands 1.., check-major: band b row r slot j at (b-1) n + r wr + j)
@@ -99,4 +118,19 @@ bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPla
 ldpc_status band_launch(const ldpc_code &c, const BandPlan &p, const float *llr, int64_t frames,
                         const ldpc_decode_opts &o, uint32_t *bits, uint8_t *syn, int32_t *iters, float *post,
                         void *ws, size_t ws_bytes, void *stream);
+
+// Launch plan of the cluster band kernel (frames larger than one SM).
+struct ClusterPlan {
+    void *kernel = nullptr;
+    int cluster = 0;
+    int threads = 0;
+    int grid = 0;
+    size_t smem = 0;
+    int64_t slot_floats = 0;
+    size_t ws_bytes = 0;
+};
+bool cluster_plan(const ldpc_code &c, int64_t frames, bool et, ClusterPlan &p);
+ldpc_status cluster_launch(const ldpc_code &c, const ClusterPlan &p, const float *llr, int64_t frames,
+                           const ldpc_decode_opts &o, uint32_t *bits, uint8_t *syn, int32_t *iters, float *post,
+                           void *ws, size_t ws_bytes, void *stream);
 }  // namespace ldpc

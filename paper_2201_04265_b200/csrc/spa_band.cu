@@ -445,7 +445,260 @@ void *pick_band_kernel(int wr, int wc, int b0, bool et, bool vm) {
     return nullptr;
 }
 
+// ---------------------------------------------------------------------------
+// Cluster band kernel: frames too large for one SM (C5: n = 64800, 1.04 MB of
+// message state).  A cluster of C CTAs decodes one frame; CTA q owns rows
+// [q mbq, (q+1) mbq) of every band and the variables of its band-0 rows, and
+// keeps their E (band 0 in registers, bands >= 1 in shared memory) and L in
+// shared memory.  Values owned by another CTA of the cluster are read from
+// the frame's global copies Lg / Eg (L2-resident; random DSMEM access was
+// measured 10-20x slower, profiles/r01_microbench.txt), which every CTA
+// refreshes with coalesced stores after each phase; a cluster barrier
+// (release/acquire) separates the phases.  Fixed-iteration mode only.
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ float ld_l_or_g(const char *smem, const float *g, int32_t idx) {
+    return idx >= 0 ? *reinterpret_cast<const float *>(smem + idx) : __ldcg(g + ~idx);
+}
+
+struct ClusterArgs {
+    DeviceCode code;
+    const float *llr;
+    int64_t frames;
+    int32_t max_iter;
+    uint32_t *bits;
+    uint8_t *syn_ok;
+    int32_t *iters;
+    float *posterior;
+    float *gstate;          // per cluster slot: Lg[n] | Eg[(wc-1) n] | Rg[n] | flags[16]
+    int64_t slot_floats;
+};
+
+template <int WR, int WC, int B0, int C>
+__global__ void __launch_bounds__(1024, 1) band_cluster_kernel(const ClusterArgs a) {
+    extern __shared__ __align__(16) char smem[];
+    const DeviceCode &code = a.code;
+    const int n = code.n, mb = code.mb;
+    const int mbq = mb / C, nq = n / C;
+    const int T = blockDim.x, tt = threadIdx.x;
+    constexpr int NB = WC - 1;
+    constexpr int B1 = NB * B0;
+    const int q = int(blockIdx.x % C);
+    const int64_t cid = blockIdx.x / C, nclusters = gridDim.x / C;
+    const uint32_t lbase = uint32_t(NB) * uint32_t(mbq) * WR * 4u;      // own L after own E_hi
+    float *Ls = reinterpret_cast<float *>(smem + lbase);
+    float *Lg = a.gstate + cid * a.slot_floats;
+    float *Eg = Lg + n;
+    float *Rg = Eg + int64_t(NB) * n;
+    int *flags = reinterpret_cast<int *>(Rg + n);
+    const int32_t *lidx = code.cband_lidx;
+    const int32_t *vpos = code.cband_vpos;
+
+    for (int64_t f = cid; f < a.frames; f += nclusters) {
+        // ingest own variables: R (log2 units) to Rg, L = R to Ls and Lg; E = 0
+        const float *src = a.llr + f * int64_t(n) + int64_t(q) * nq;
+        for (int v4 = tt; v4 < (nq >> 2); v4 += T) {
+            float4 r = __ldg(reinterpret_cast<const float4 *>(src) + v4);
+            r.x = fminf(fmaxf(r.x, -30.0f), 30.0f) * kL2E;
+            r.y = fminf(fmaxf(r.y, -30.0f), 30.0f) * kL2E;
+            r.z = fminf(fmaxf(r.z, -30.0f), 30.0f) * kL2E;
+            r.w = fminf(fmaxf(r.w, -30.0f), 30.0f) * kL2E;
+            reinterpret_cast<float4 *>(Ls)[v4] = r;
+            reinterpret_cast<float4 *>(Lg + int64_t(q) * nq)[v4] = r;
+            reinterpret_cast<float4 *>(Rg + int64_t(q) * nq)[v4] = r;
+        }
+        for (int i = tt; i < int(lbase >> 4); i += T) reinterpret_cast<float4 *>(smem)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        float e0[B0][WR];
+#pragma unroll
+        for (int k = 0; k < B0; ++k)
+#pragma unroll
+            for (int j = 0; j < WR; ++j) e0[k][j] = 0.0f;
+        cluster_sync_all();
+
+        for (int t = 1; t <= a.max_iter; ++t) {
+            // check phase over own rows
+#pragma unroll
+            for (int k = 0; k < B0; ++k) {
+                const int r = tt + k * T;
+                if (r < mbq) {
+                    float lv[WR], x[WR];
+                    lds_row<WR>(reinterpret_cast<const char *>(Ls), uint32_t(r) * WR * 4u, lv);
+#pragma unroll
+                    for (int j = 0; j < WR; ++j) x[j] = lv[j] - e0[k][j];
+                    check_row<WR, true>(x, e0[k]);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < B1; ++k) {
+                const int r = tt + k * T;                 // local row over bands >= 1
+                if (r < NB * mbq) {
+                    const int b = r / mbq, lr = r - b * mbq;
+                    const int64_t gpos = int64_t(b) * n + int64_t(q * mbq + lr) * WR;   // Eg / lidx position
+                    int32_t li[WR];
+                    float e[WR], x[WR];
+                    ldg_idx<WR>(lidx + gpos, li);
+                    lds_row<WR>(smem, uint32_t(r) * WR * 4u, e);
+#pragma unroll
+                    for (int j = 0; j < WR; ++j) x[j] = ld_l_or_g(smem, Lg, li[j]) - e[j];
+                    check_row<WR, true>(x, e);
+                    sts_row<WR>(smem, uint32_t(r) * WR * 4u, e);
+                    sts_row<WR>(reinterpret_cast<char *>(Eg + gpos), 0u, e);
+                }
+            }
+            cluster_sync_all();
+            // variable phase over own variables
+#pragma unroll
+            for (int k = 0; k < B0; ++k) {
+                const int r = tt + k * T;
+                if (r < mbq) {
+                    const int64_t v0 = int64_t(q * mbq + r) * WR;
+                    float rv[WR], lv[WR];
+                    int32_t vp[WR * NB];
+                    lds_row<WR>(reinterpret_cast<const char *>(Rg + v0), 0u, rv);
+                    ldg_idx<WR * NB>(vpos + v0 * NB, vp);
+#pragma unroll
+                    for (int j = 0; j < WR; ++j) {
+                        float s = rv[j] + e0[k][j];
+#pragma unroll
+                        for (int b = 0; b < NB; ++b) s += ld_l_or_g(smem, Eg, vp[j * NB + b]);
+                        lv[j] = s;
+                    }
+                    sts_row<WR>(reinterpret_cast<char *>(Ls), uint32_t(r) * WR * 4u, lv);
+                    sts_row<WR>(reinterpret_cast<char *>(Lg + v0), 0u, lv);
+                }
+            }
+            cluster_sync_all();
+        }
+        // syndrome of z = [L >= 0] over own rows, OR-ed across the cluster
+        uint32_t synd = 0;
+        for (int r = tt; r < mbq; r += T)
+            for (int j = 0; j < WR; ++j) synd ^= (Ls[r * WR + j] >= 0.0f) ? 1u : 0u;
+        for (int r = tt; r < NB * mbq; r += T) {
+            const int b = r / mbq, lr = r - b * mbq;
+            const int64_t gpos = int64_t(b) * n + int64_t(q * mbq + lr) * WR;
+            for (int j = 0; j < WR; ++j) synd ^= (ld_l_or_g(smem, Lg, __ldg(lidx + gpos + j)) >= 0.0f) ? 1u : 0u;
+        }
+        const int any = __syncthreads_or(synd != 0);
+        if (tt == 0) flags[q] = any;
+        cluster_sync_all();
+        // outputs: CTA q writes a word-aligned slice of the frame's bits
+        const int nw = code.nw;
+        const int wper = (nw + C - 1) / C;
+        const int w0 = q * wper, w1 = min(nw, w0 + wper);
+        uint32_t *bits = a.bits + f * int64_t(nw);
+        for (int v = w0 * 32 + tt; v < w1 * 32; v += T) {
+            const bool z = (v < n) ? (__ldcg(Lg + v) >= 0.0f) : false;
+            const uint32_t word = __ballot_sync(0xffffffffu, z);
+            if ((tt & 31) == 0) bits[v >> 5] = word;
+        }
+        if (a.posterior) {
+            float *dst = a.posterior + f * int64_t(n) + int64_t(q) * nq;
+            for (int v = tt; v < nq; v += T) dst[v] = Ls[v] * kLn2;
+        }
+        if (q == 0 && tt == 0) {
+            int ok = 1;
+            for (int i = 0; i < C; ++i) ok &= (__ldcg(flags + i) == 0);
+            a.syn_ok[f] = uint8_t(ok);
+            a.iters[f] = a.max_iter;
+        }
+        cluster_sync_all();     // Lg / flags are reused by the next frame
+    }
+}
+
+template <int WR, int B0>
+void *pick_cluster_c(int C) {
+    switch (C) {
+        case 2: return reinterpret_cast<void *>(&band_cluster_kernel<WR, 3, B0, 2>);
+        case 4: return reinterpret_cast<void *>(&band_cluster_kernel<WR, 3, B0, 4>);
+        case 8: return reinterpret_cast<void *>(&band_cluster_kernel<WR, 3, B0, 8>);
+    }
+    return nullptr;
+}
+
+void *pick_cluster_kernel(int wr, int wc, int b0, int C) {
+    if (wc != 3 || wr != 6) return nullptr;
+    switch (b0) {
+        case 1: return pick_cluster_c<6, 1>(C);
+        case 2: return pick_cluster_c<6, 2>(C);
+        case 3: return pick_cluster_c<6, 3>(C);
+    }
+    return nullptr;
+}
+
 }  // namespace
+
+bool cluster_plan(const ldpc_code &c, int64_t frames, bool et, ClusterPlan &p) {
+    if (et || !c.gallager || !c.regular_col || (c.n & 3)) return false;
+    const int C = band_cluster_size(c.n, c.wc, c.wr);
+    if (C == 0) return false;
+    const int mbq = c.n / c.wr / C, nq = c.n / C;
+    if (nq & 3) return false;
+    const int b0 = std::max(1, (mbq + 1023) / 1024);
+    void *k = pick_cluster_kernel(c.wr, c.wc, b0, C);
+    if (!k) return false;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    p.kernel = k;
+    p.cluster = C;
+    p.threads = ((mbq + b0 - 1) / b0 + 31) / 32 * 32;
+    p.smem = size_t(c.wc) * size_t(nq) * 4;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p.smem)) != cudaSuccess) return false;
+    if (C > 8 && cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) return false;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(C);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(unsigned(C));
+    cfg.blockDim = dim3(unsigned(p.threads));
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, k, &cfg) != cudaSuccess || nclusters < 1) return false;
+    nclusters = int(std::min<int64_t>(nclusters, std::max<int64_t>(frames, 1)));
+    p.grid = nclusters * C;
+    p.slot_floats = (int64_t(c.wc + 1) * c.n + 16 + 63) & ~int64_t(63);
+    p.ws_bytes = size_t(nclusters) * size_t(p.slot_floats) * 4;
+    (void)sms;
+    return true;
+}
+
+ldpc_status cluster_launch(const ldpc_code &c, const ClusterPlan &p, const float *llr, int64_t frames,
+                           const ldpc_decode_opts &o, uint32_t *bits, uint8_t *syn, int32_t *iters, float *post,
+                           void *ws, size_t ws_bytes, void *stream) {
+    if (!ws || ws_bytes < p.ws_bytes) return LDPC_ERR_ARG;
+    ClusterArgs a;
+    a.code = c.dev;
+    a.llr = llr;
+    a.frames = frames;
+    a.max_iter = o.max_iter;
+    a.bits = bits;
+    a.syn_ok = syn;
+    a.iters = iters;
+    a.posterior = post;
+    a.gstate = static_cast<float *>(ws);
+    a.slot_floats = p.slot_floats;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(p.cluster);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(unsigned(p.grid));
+    cfg.blockDim = dim3(unsigned(p.threads));
+    cfg.dynamicSmemBytes = p.smem;
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    void *args[] = {&a};
+    cudaError_t e = cudaLaunchKernelExC(&cfg, p.kernel, args);
+    return e == cudaSuccess ? LDPC_OK : LDPC_ERR_CUDA;
+}
 
 bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPlan &p) {
     if (!c.gallager || !c.regular_col || (c.n & 3)) return false;

@@ -485,6 +485,14 @@ ldpc_status ldpc_decode_workspace_bytes(const ldpc_code *code, int64_t frames, c
         }
         if (opts->variant != 0) return LDPC_ERR_UNSUPPORTED;
     }
+    if (opts->variant == 0 || opts->variant == 5) {
+        ldpc::ClusterPlan cp;
+        if (ldpc::cluster_plan(*code, std::max<int64_t>(frames, 1), opts->early_term != 0, cp)) {
+            *bytes = cp.ws_bytes;
+            return LDPC_OK;
+        }
+        if (opts->variant == 5) return LDPC_ERR_UNSUPPORTED;
+    }
     ldpc::Plan p;
     ldpc_status s = ldpc::make_plan(*code, std::max<int64_t>(frames, 1), *opts, p);
     if (s != LDPC_OK) return s;
@@ -507,6 +515,13 @@ ldpc_status ldpc_decode(const ldpc_code *code, const float *d_llr, int64_t frame
             return ldpc::band_launch(*code, bp, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters, d_posterior,
                                      d_ws, ws_bytes, stream);
         if (opts->variant != 0) return LDPC_ERR_UNSUPPORTED;
+    }
+    if (opts->variant == 0 || opts->variant == 5) {
+        ldpc::ClusterPlan cp;
+        if (ldpc::cluster_plan(*code, frames, opts->early_term != 0, cp))
+            return ldpc::cluster_launch(*code, cp, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters,
+                                        d_posterior, d_ws, ws_bytes, stream);
+        if (opts->variant == 5) return LDPC_ERR_UNSUPPORTED;
     }
     ldpc::Plan p;
     ldpc_status s = ldpc::make_plan(*code, frames, *opts, p);
