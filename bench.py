@@ -393,7 +393,8 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clocks,
-            "gpu_launches": 3 * args.steps,
+            # per step: encode_parity + encode_assemble + decode + count
+            "gpu_launches": 4 * args.steps,
             "setup_s": setup_s,
         }
         print(json.dumps(line), flush=True)

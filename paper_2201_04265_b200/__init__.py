@@ -151,6 +151,14 @@ def _opts(max_iter: int, early_term: bool, variant: int) -> DecodeOpts:
     return DecodeOpts(int(max_iter), int(bool(early_term)), int(variant), 0)
 
 
+def ldpc_decode_variant(code: Code, frames: int, max_iter: int = 50, early_term: bool = False,
+                        variant: int = 0) -> int:
+    o = _opts(max_iter, early_term, variant)
+    out = C.c_int32(0)
+    call("ldpc_decode_variant", code.handle, int(frames), C.byref(o), C.byref(out))
+    return int(out.value)
+
+
 def ldpc_decode_workspace_bytes(code: Code, frames: int, max_iter: int = 50, early_term: bool = False,
                                 variant: int = 0) -> int:
     o = _opts(max_iter, early_term, variant)

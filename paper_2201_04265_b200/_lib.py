@@ -18,6 +18,7 @@ EXPORTED = [
     "ldpc_make_H", "ldpc_code_from_csr", "ldpc_make_G", "ldpc_code_query", "ldpc_code_copy_H",
     "ldpc_code_copy_csr", "ldpc_code_copy_perm", "ldpc_code_copy_P", "ldpc_code_bind_device",
     "ldpc_code_free", "ldpc_status_str", "ldpc_encode", "ldpc_decode_workspace_bytes", "ldpc_decode",
+    "ldpc_decode_variant",
     "ldpc_gen_info", "ldpc_channel", "ldpc_count_errors", "ldpc_partition", "ldpc_debug_phi",
 ]
 
@@ -62,6 +63,7 @@ def lib() -> C.CDLL:
             "ldpc_code_bind_device": [vp, vp, sz, vp],
             "ldpc_encode": [vp, vp, vp, i64, vp],
             "ldpc_decode_workspace_bytes": [vp, i64, vp, vp],
+            "ldpc_decode_variant": [vp, i64, vp, vp],
             "ldpc_decode": [vp, vp, i64, vp, vp, vp, vp, vp, vp, sz, vp],
             "ldpc_gen_info": [u64, i64, i64, i32, vp, vp],
             "ldpc_channel": [vp, u64, i64, i64, vp, C.c_double, vp, vp],

@@ -22,6 +22,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "ldpc_internal.h"
 
@@ -659,7 +661,14 @@ bool cluster_plan(const ldpc_code &c, int64_t frames, bool et, ClusterPlan &p) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int nclusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclusters, k, &cfg) != cudaSuccess || nclusters < 1) return false;
+    const cudaError_t oe = cudaOccupancyMaxActiveClusters(&nclusters, k, &cfg);
+    if (oe != cudaSuccess || nclusters < 1) {
+        if (std::getenv("LDPC_DEBUG"))
+            std::fprintf(stderr, "ldpc cluster_plan: occupancy query: %s, clusters %d (C=%d, threads %d, smem %zu)\n",
+                         cudaGetErrorString(oe), nclusters, C, p.threads, p.smem);
+        cudaGetLastError();
+        return false;
+    }
     nclusters = int(std::min<int64_t>(nclusters, std::max<int64_t>(frames, 1)));
     p.grid = nclusters * C;
     p.slot_floats = (int64_t(c.wc + 1) * c.n + 16 + 63) & ~int64_t(63);

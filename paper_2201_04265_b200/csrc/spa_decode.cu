@@ -474,6 +474,34 @@ ldpc_status make_plan(const ldpc_code &c, int64_t frames, const ldpc_decode_opts
 
 extern "C" {
 
+ldpc_status ldpc_decode_variant(const ldpc_code *code, int64_t frames, const ldpc_decode_opts *opts,
+                                int32_t *variant) {
+    if (!code || !opts || !variant || frames < 0) return LDPC_ERR_ARG;
+    *variant = 0;
+    frames = std::max<int64_t>(frames, 1);
+    if (opts->variant == 0 || opts->variant == 3 || opts->variant == 4) {
+        ldpc::BandPlan bp;
+        if (ldpc::band_plan(*code, frames, opts->early_term != 0, opts->variant, bp)) {
+            *variant = bp.vm ? 4 : 3;
+            return LDPC_OK;
+        }
+        if (opts->variant != 0) return LDPC_ERR_UNSUPPORTED;
+    }
+    if (opts->variant == 0 || opts->variant == 5) {
+        ldpc::ClusterPlan cp;
+        if (ldpc::cluster_plan(*code, frames, opts->early_term != 0, cp)) {
+            *variant = 5;
+            return LDPC_OK;
+        }
+        if (opts->variant == 5) return LDPC_ERR_UNSUPPORTED;
+    }
+    ldpc::Plan p;
+    ldpc_status s = ldpc::make_plan(*code, frames, *opts, p);
+    if (s != LDPC_OK) return s;
+    *variant = p.variant;
+    return LDPC_OK;
+}
+
 ldpc_status ldpc_decode_workspace_bytes(const ldpc_code *code, int64_t frames, const ldpc_decode_opts *opts,
                                         size_t *bytes) {
     if (!code || !opts || !bytes || frames < 0) return LDPC_ERR_ARG;
