@@ -85,6 +85,9 @@ DeviceLayout compute_layout(const ldpc_code &c, bool with_G) {
         const size_t nb = size_t(c.wc - 1) * size_t(c.n);
         L.band_lidx = off; off = align256(off + sizeof(int32_t) * nb);
         L.band_vpos = off; off = align256(off + sizeof(int32_t) * nb);
+        if (c.n <= 16383) {
+            L.band_lidx16 = off; off = align256(off + sizeof(uint16_t) * nb);
+        }
         if (band_cluster_size(c.n, c.wc, c.wr) > 0) {
             L.cband_lidx = off; off = align256(off + sizeof(int32_t) * nb);
             L.cband_vpos = off; off = align256(off + sizeof(int32_t) * nb);
@@ -367,6 +370,12 @@ ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, vo
             }
         ok = put(L.band_lidx, lidx.data(), sizeof(int32_t) * lidx.size()) &&
              put(L.band_vpos, vpos.data(), sizeof(int32_t) * vpos.size());
+        std::vector<uint16_t> l16;
+        if (ok && n <= 16383) {
+            l16.resize(lidx.size());
+            for (size_t e = 0; e < lidx.size(); ++e) l16[e] = uint16_t(size_t(lidx[e]) - lbase);
+            ok = put(L.band_lidx16, l16.data(), sizeof(uint16_t) * l16.size());
+        }
         const int C = ldpc::band_cluster_size(n, wc, code->wr);
         if (ok && C > 0) {
             // CTA q of a cluster owns band rows [q mbq, (q+1) mbq) of every band and
@@ -415,6 +424,8 @@ ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, vo
     D.mb = code->gallager ? code->n / code->wr : 0;
     D.band_lidx = (code->gallager && code->wc >= 2) ? reinterpret_cast<const int32_t *>(base + L.band_lidx) : nullptr;
     D.band_vpos = (code->gallager && code->wc >= 2) ? reinterpret_cast<const int32_t *>(base + L.band_vpos) : nullptr;
+    D.band_lidx16 = (code->gallager && code->wc >= 2 && code->n <= 16383)
+                        ? reinterpret_cast<const uint16_t *>(base + L.band_lidx16) : nullptr;
     D.cluster = (code->gallager && code->wc >= 2) ? ldpc::band_cluster_size(code->n, code->wc, code->wr) : 0;
     D.cband_lidx = D.cluster ? reinterpret_cast<const int32_t *>(base + L.cband_lidx) : nullptr;
     D.cband_vpos = D.cluster ? reinterpret_cast<const int32_t *>(base + L.cband_vpos) : nullptr;

@@ -29,6 +29,7 @@ struct DeviceLayout {
     // Gallager band view (ldpc_make_H codes only), used by the band kernel:
     size_t band_lidx = 0;  // int32 [(wc-1)*n]  edge (band b>=1, position p) -> byte offset of L[pi_b[p]]
     size_t band_vpos = 0;  // int32 [n*(wc-1)]  variable v, band b>=1 -> byte offset of its E in E_hi
+    size_t band_lidx16 = 0; // uint16 [(wc-1)*n] 4*v (n <= 16383): band_lidx - L base, half the bytes
     // Cluster band view (frames too large for one SM: C CTAs share a frame):
     // value >= 0: byte offset in the owning CTA's shared memory; value < 0:
     // ~(element index) into the frame's global copy (Lg for lidx, Eg for vpos).
@@ -55,7 +56,8 @@ struct DeviceCode {
     int32_t gallager, wc, wr, mb;   // band structure (mb = n / wr rows per band)
     const int32_t *band_lidx;
     const int32_t *band_vpos;
-    int32_t cluster;                // C of the cluster band view (0: none)
+    const uint16_t *band_lidx16;    // null when n > 16383
+    int32_t cluster;               // C of the cluster band view (0: none)
     const int32_t *cband_lidx;
     const int32_t *cband_vpos;
 };
@@ -109,6 +111,7 @@ struct BandPlan {
     size_t smem = 0;
     bool r_in_smem = false;
     bool vm = false;            // E of bands >= 1 stored variable-major
+    int mode = 0;               // kernel MODE: 0 check-major, 1 VM, 2 VM + 16-bit offsets
     size_t ws_bytes = 0;
 };
 // false when the code is not eligible (not from ldpc_make_H, unsupported

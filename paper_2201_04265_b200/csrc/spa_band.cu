@@ -235,8 +235,10 @@ __device__ __forceinline__ bool cta_sync_or(bool p) { return __syncthreads_or(p 
 // WR: row weight, WC: column weight (bands), B0: max band-0 rows per thread.
 // wc > 3 (Table I codes, n = 1032) use small CTAs: the 256-thread bound leaves
 // room for the wider per-row state.
-template <int WR, int WC, int B0, bool ET, bool VM>
+// MODE 0: check-major E; 1: variable-major E (VM); 2: VM + 16-bit L offsets.
+template <int WR, int WC, int B0, bool ET, int MODE>
 __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const BandArgs a) {
+    constexpr bool VM = MODE >= 1, L16 = MODE == 2;
     extern __shared__ __align__(16) char smem[];
     __shared__ long long s_frame;
     const DeviceCode &code = a.code;
@@ -302,7 +304,18 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
                 if (tt < S && r < NB * mb) {
                     int32_t li[WR];
                     float e[WR], x[WR];
-                    ldg_idx<WR>(lidx + size_t(r) * WR, li);
+                    if (L16) {
+                        // 16-bit offsets relative to L: half the index bytes through L1/L2
+                        const uint32_t *p16 = reinterpret_cast<const uint32_t *>(code.band_lidx16 + size_t(r) * WR);
+#pragma unroll
+                        for (int w = 0; w < WR / 2; ++w) {
+                            const uint32_t x = __ldg(p16 + w);
+                            li[2 * w] = int32_t(lbase + (x & 0xffffu));
+                            li[2 * w + 1] = int32_t(lbase + (x >> 16));
+                        }
+                    } else {
+                        ldg_idx<WR>(lidx + size_t(r) * WR, li);
+                    }
                     // VM: E_b is variable-major, at the variable's L offset + delta_b
                     const int32_t delta = VM ? int32_t((r / mb) * n * 4) - int32_t(lbase) : 0;
                     if (VM) {
@@ -402,16 +415,19 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
 }
 
 template <int WR, int WC, int B0>
-void *pick_et(bool et, bool vm) {
-    if (vm)
-        return et ? reinterpret_cast<void *>(&band_kernel<WR, WC, B0, true, true>)
-                  : reinterpret_cast<void *>(&band_kernel<WR, WC, B0, false, true>);
-    return et ? reinterpret_cast<void *>(&band_kernel<WR, WC, B0, true, false>)
-              : reinterpret_cast<void *>(&band_kernel<WR, WC, B0, false, false>);
+void *pick_et(bool et, int mode) {
+    if (mode == 2)
+        return et ? reinterpret_cast<void *>(&band_kernel<WR, WC, B0, true, 2>)
+                  : reinterpret_cast<void *>(&band_kernel<WR, WC, B0, false, 2>);
+    if (mode == 1)
+        return et ? reinterpret_cast<void *>(&band_kernel<WR, WC, B0, true, 1>)
+                  : reinterpret_cast<void *>(&band_kernel<WR, WC, B0, false, 1>);
+    return et ? reinterpret_cast<void *>(&band_kernel<WR, WC, B0, true, 0>)
+              : reinterpret_cast<void *>(&band_kernel<WR, WC, B0, false, 0>);
 }
 
 template <int WR, int WC>
-void *pick_b0(int b0, bool et, bool vm) {
+void *pick_b0(int b0, bool et, int vm) {
     switch (b0) {
         case 1: return pick_et<WR, WC, 1>(et, vm);
         case 2: return pick_et<WR, WC, 2>(et, vm);
@@ -422,7 +438,7 @@ void *pick_b0(int b0, bool et, bool vm) {
 }
 
 template <int WR, int WC>
-void *pick_b0_small(int b0, bool et, bool vm) {
+void *pick_b0_small(int b0, bool et, int vm) {
     switch (b0) {
         case 1: return pick_et<WR, WC, 1>(et, vm);
         case 2: return pick_et<WR, WC, 2>(et, vm);
@@ -432,7 +448,7 @@ void *pick_b0_small(int b0, bool et, bool vm) {
 
 // (wc, wr) instantiated: the BASELINE.json configs ((3, 4), (3, 6), (3, 12))
 // and the paper's Table I (wr = 12 with wc = 9, 6, 3).
-void *pick_band_kernel(int wr, int wc, int b0, bool et, bool vm) {
+void *pick_band_kernel(int wr, int wc, int b0, bool et, int vm) {
     if (wc == 3) {
         switch (wr) {
             case 4: return pick_b0<4, 3>(b0, et, vm);
@@ -725,8 +741,10 @@ bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPla
     p.r_in_smem = with_r + reserve <= size_t(optin);
     // Variable-major E (variant 4) drops the variable phase's index loads and
     // gathers; it pays off when the indices no longer fit in L1 (large n).
-    p.vm = variant == 4 || (variant == 0 && (!p.r_in_smem || c.wc > 3));
-    void *k = pick_band_kernel(c.wr, c.wc, b0, et, p.vm);
+    p.vm = variant == 4 || variant == 6 || (variant == 0 && (!p.r_in_smem || c.wc > 3));
+    // 16-bit offsets (variant 6, auto with VM when n <= 16383): +2% on C4
+    p.mode = p.vm ? (((variant == 6 || variant == 0) && c.n <= 16383) ? 2 : 1) : 0;
+    void *k = pick_band_kernel(c.wr, c.wc, b0, et, p.mode);
     if (!k) return false;
     cudaFuncAttributes fa;
     if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) return false;

@@ -479,10 +479,10 @@ ldpc_status ldpc_decode_variant(const ldpc_code *code, int64_t frames, const ldp
     if (!code || !opts || !variant || frames < 0) return LDPC_ERR_ARG;
     *variant = 0;
     frames = std::max<int64_t>(frames, 1);
-    if (opts->variant == 0 || opts->variant == 3 || opts->variant == 4) {
+    if (opts->variant == 0 || opts->variant == 3 || opts->variant == 4 || opts->variant == 6) {
         ldpc::BandPlan bp;
         if (ldpc::band_plan(*code, frames, opts->early_term != 0, opts->variant, bp)) {
-            *variant = bp.vm ? 4 : 3;
+            *variant = bp.mode == 2 ? 6 : (bp.vm ? 4 : 3);
             return LDPC_OK;
         }
         if (opts->variant != 0) return LDPC_ERR_UNSUPPORTED;
@@ -505,7 +505,7 @@ ldpc_status ldpc_decode_variant(const ldpc_code *code, int64_t frames, const ldp
 ldpc_status ldpc_decode_workspace_bytes(const ldpc_code *code, int64_t frames, const ldpc_decode_opts *opts,
                                         size_t *bytes) {
     if (!code || !opts || !bytes || frames < 0) return LDPC_ERR_ARG;
-    if (opts->variant == 0 || opts->variant == 3 || opts->variant == 4) {
+    if (opts->variant == 0 || opts->variant == 3 || opts->variant == 4 || opts->variant == 6) {
         ldpc::BandPlan bp;
         if (ldpc::band_plan(*code, std::max<int64_t>(frames, 1), opts->early_term != 0, opts->variant, bp)) {
             *bytes = bp.ws_bytes;
@@ -537,7 +537,7 @@ ldpc_status ldpc_decode(const ldpc_code *code, const float *d_llr, int64_t frame
     if (frames == 0) return LDPC_OK;
     if (!d_llr || !d_bits || !d_syndrome_ok || !d_iters) return LDPC_ERR_ARG;
     if (reinterpret_cast<uintptr_t>(d_llr) & 15u) return LDPC_ERR_ARG;
-    if (opts->variant == 0 || opts->variant == 3 || opts->variant == 4) {
+    if (opts->variant == 0 || opts->variant == 3 || opts->variant == 4 || opts->variant == 6) {
         ldpc::BandPlan bp;
         if (ldpc::band_plan(*code, frames, opts->early_term != 0, opts->variant, bp))
             return ldpc::band_launch(*code, bp, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters, d_posterior,
