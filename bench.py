@@ -267,14 +267,11 @@ def main():
     import paper_2201_04265_b200 as L
     from paper_2201_04265_b200 import dist as LD
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
+    rank, world, local = LD.world()
+    launched = "RANK" in os.environ and "MASTER_ADDR" in os.environ     # under torchrun
+    torch.cuda.set_device(local if launched else 0)
+    if launched:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
     wl = W.ALL[args.config]
     frames = args.frames or (wl.frames if wl.frames * wl.n * 4 < 40e9 else 16384)
@@ -315,7 +312,7 @@ def main():
         ev_d1.record(stream)
         d_ctr.zero_()
         L.ldpc_count_errors(code, d_info, d_bits, d_cw, d_syn, d_it, frames, d_ctr)
-        if world > 1:
+        if launched:
             LD.all_reduce_counters(d_ctr)
 
     ev_d0 = torch.cuda.Event(enable_timing=True)
@@ -325,7 +322,7 @@ def main():
     torch.cuda.synchronize()
 
     # ---- timed region
-    if world > 1:
+    if launched:
         dist.barrier()
     torch.cuda.synchronize()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -340,12 +337,12 @@ def main():
             ends[i].synchronize()
             dec_ms.append(ev_d0.elapsed_time(ev_d1))
         torch.cuda.synchronize()
-    if world > 1:
+    if launched:
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = sum(step_ms)
     t = torch.tensor([total_ms, sum(dec_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
+    if launched:
         LD.max_over_ranks(t)
     total_ms, dec_total_ms = float(t[0]), float(t[1])
     ctr = d_ctr.cpu().numpy()
@@ -398,7 +395,7 @@ def main():
             "setup_s": setup_s,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if launched:
         dist.destroy_process_group()
     return 0
 
