@@ -219,7 +219,8 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "long double (x87 f80)",
         "data": "synthetic (seeded Philox frames, BASELINE.json recipe)",
-        "config": workload_config(wl, F, args.gpus),
+        # same config as our arm; each timed step is the bounded sample in cpu_baseline.sample
+        "config": workload_config(wl, args.frames or wl.frames, args.gpus),
         "cpu_baseline": {"value": value, "unit": "Gbit/s", "cores": threads, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
