@@ -130,7 +130,8 @@ ldpc_status ldpc_encode(const ldpc_code *code, const uint32_t *d_info, uint32_t 
 
 /* The decoder variant ldpc_decode would run for these arguments (opts->variant
  * 0 resolved): 1 generic on-chip, 2 generic global-state, 3/4 Gallager band
- * kernel (check-/variable-major E), 5 cluster band kernel.  *variant = 0 and
+ * kernel (check-/variable-major E), 5 cluster band kernel, 6 band kernel with
+ * 16-bit offsets, 7 exchange cluster kernel.  *variant = 0 and
  * LDPC_ERR_UNSUPPORTED when nothing fits. */
 ldpc_status ldpc_decode_variant(const ldpc_code *code, int64_t frames, const ldpc_decode_opts *opts,
                                 int32_t *variant);
@@ -156,7 +157,11 @@ ldpc_status ldpc_decode_workspace_bytes(const ldpc_code *code, int64_t frames,
  * global-state (CTA per frame, any n); 3 Gallager band kernel, check-major E;
  * 4 Gallager band kernel, variable-major E (3 and 4 need an ldpc_make_H code
  * whose frame fits one SM; LDPC_ERR_UNSUPPORTED otherwise); 5 cluster band
- * kernel (ldpc_make_H codes too large for one SM, wr = 6, fixed iterations). */
+ * kernel (ldpc_make_H codes too large for one SM, wr = 6, fixed iterations;
+ * remote messages through L2-resident global copies); 6 = 4 with 16-bit
+ * offsets (n <= 16383); 7 exchange cluster kernel (same codes as 5; a
+ * cluster of C CTAs per frame trades message segments with bulk DSMEM copies,
+ * no workspace; preferred by auto). */
 ldpc_status ldpc_decode(const ldpc_code *code, const float *d_llr, int64_t frames,
                         const ldpc_decode_opts *opts, uint32_t *d_bits,
                         uint8_t *d_syndrome_ok, int32_t *d_iters, float *d_posterior,

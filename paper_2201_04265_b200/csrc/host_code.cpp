@@ -92,6 +92,11 @@ DeviceLayout compute_layout(const ldpc_code &c, bool with_G) {
             L.cband_lidx = off; off = align256(off + sizeof(int32_t) * nb);
             L.cband_vpos = off; off = align256(off + sizeof(int32_t) * nb);
         }
+        if (const int C = xband_cluster_size(c.n, c.wc, c.wr)) {
+            L.xband_ridx = off; off = align256(off + sizeof(uint16_t) * nb);
+            L.xband_sidx = off; off = align256(off + sizeof(uint16_t) * nb);
+            L.xband_seg = off;  off = align256(off + sizeof(int32_t) * 3 * size_t(C) * size_t(C));
+        }
     }
     if (with_G) {
         size_t kw = (size_t(c.k) + 31) / 32;
@@ -102,6 +107,52 @@ DeviceLayout compute_layout(const ldpc_code &c, bool with_G) {
     }
     L.total = off;
     return L;
+}
+
+// Message-segment tables of the exchange cluster kernel (spa_cluster.cu).
+// CTA q owns band rows [q mbq, (q+1) mbq) of every band and the variables
+// [q nq, (q+1) nq) of its band-0 rows.  Every band-b >= 1 edge (b, p) joins
+// row owner d = (p / wr) / mbq and variable owner s = pi_b[p] / nq.  Its two
+// messages per iteration travel in segment (s, d): L_vc from s to d, E_cv
+// back from d to s, at the same rank r inside the segment (segments hold
+// their edges in ascending (b, p)).  A CTA's buffer laid out by destination
+// ("send layout", its variables' edges) puts segment (s, d) at sOff[s][d]; laid
+// out by source ("receive layout", its rows' edges) puts it at rOff[s][d].
+// Segments are padded to 16 bytes (bulk-copy granularity).
+//   ridx[(b-1) n + p]    = rOff[s][d] + 4 r   (byte slot in d's buffer)
+//   sidx[v (wc-1) + b-1] = sOff[s][d] + 4 r   (byte slot in s's buffer)
+//   seg = { sOff, rOff, bytes } as three C x C int32 arrays indexed [s][d].
+void xband_tables(const ldpc_code &c, int C, std::vector<uint16_t> &ridx, std::vector<uint16_t> &sidx,
+                  std::vector<int32_t> &seg) {
+    const int32_t n = c.n, wc = c.wc, wr = c.wr, mbq = n / wr / C, nq = n / C;
+    const size_t nb = size_t(wc - 1) * size_t(n);
+    std::vector<int32_t> cnt(size_t(C) * C, 0), rank(nb);
+    for (int32_t b = 1; b < wc; ++b)
+        for (int32_t p = 0; p < n; ++p) {
+            const int32_t d = (p / wr) / mbq, s = c.col_idx[size_t(b) * n + p] / nq;
+            rank[size_t(b - 1) * n + p] = cnt[size_t(s) * C + d]++;
+        }
+    auto pad = [](int32_t x) { return (x + 3) & ~3; };
+    seg.assign(3 * size_t(C) * C, 0);
+    int32_t *sOff = seg.data(), *rOff = seg.data() + C * C, *bytes = seg.data() + 2 * C * C;
+    for (int32_t s = 0; s < C; ++s) {
+        int32_t o = 0;
+        for (int32_t d = 0; d < C; ++d) { sOff[s * C + d] = 4 * o; o += pad(cnt[size_t(s) * C + d]); }
+    }
+    for (int32_t d = 0; d < C; ++d) {
+        int32_t o = 0;
+        for (int32_t s = 0; s < C; ++s) { rOff[s * C + d] = 4 * o; o += pad(cnt[size_t(s) * C + d]); }
+    }
+    for (int32_t i = 0; i < C * C; ++i) bytes[i] = 4 * pad(cnt[i]);
+    ridx.assign(nb, 0);
+    sidx.assign(nb, 0);
+    for (int32_t b = 1; b < wc; ++b)
+        for (int32_t p = 0; p < n; ++p) {
+            const int32_t v = c.col_idx[size_t(b) * n + p];
+            const int32_t d = (p / wr) / mbq, s = v / nq, r = rank[size_t(b - 1) * n + p];
+            ridx[size_t(b - 1) * n + p] = uint16_t(rOff[s * C + d] + 4 * r);
+            sidx[size_t(v) * (wc - 1) + (b - 1)] = uint16_t(sOff[s * C + d] + 4 * r);
+        }
 }
 }  // namespace ldpc
 
@@ -396,6 +447,15 @@ ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, vo
             ok = put(L.cband_lidx, lidx.data(), sizeof(int32_t) * lidx.size()) &&
                  put(L.cband_vpos, vpos.data(), sizeof(int32_t) * vpos.size());
         }
+        const int X = ldpc::xband_cluster_size(n, wc, code->wr);
+        if (ok && X > 0) {
+            std::vector<uint16_t> ridx, sidx;
+            std::vector<int32_t> seg;
+            ldpc::xband_tables(*code, X, ridx, sidx, seg);
+            ok = put(L.xband_ridx, ridx.data(), sizeof(uint16_t) * ridx.size()) &&
+                 put(L.xband_sidx, sidx.data(), sizeof(uint16_t) * sidx.size()) &&
+                 put(L.xband_seg, seg.data(), sizeof(int32_t) * seg.size());
+        }
     }
     if (ok && code->has_G)
         ok = put(L.perm, code->perm.data(), sizeof(int32_t) * code->perm.size()) &&
@@ -429,6 +489,11 @@ ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, vo
     D.cluster = (code->gallager && code->wc >= 2) ? ldpc::band_cluster_size(code->n, code->wc, code->wr) : 0;
     D.cband_lidx = D.cluster ? reinterpret_cast<const int32_t *>(base + L.cband_lidx) : nullptr;
     D.cband_vpos = D.cluster ? reinterpret_cast<const int32_t *>(base + L.cband_vpos) : nullptr;
+    D.xcluster = (code->gallager && code->wc >= 2) ? ldpc::xband_cluster_size(code->n, code->wc, code->wr) : 0;
+    D.xcap = D.xcluster ? ldpc::xband_capacity(code->n, code->wc, D.xcluster) : 0;
+    D.xband_ridx = D.xcluster ? reinterpret_cast<const uint16_t *>(base + L.xband_ridx) : nullptr;
+    D.xband_sidx = D.xcluster ? reinterpret_cast<const uint16_t *>(base + L.xband_sidx) : nullptr;
+    D.xband_seg = D.xcluster ? reinterpret_cast<const int32_t *>(base + L.xband_seg) : nullptr;
     D.pt = code->has_G ? reinterpret_cast<const uint32_t *>(base + L.pt) : nullptr;
     D.npar_pad = code->has_G ? (code->n - code->k + ldpc::kEncColTile - 1) / ldpc::kEncColTile * ldpc::kEncColTile : 0;
     return LDPC_OK;

@@ -35,6 +35,12 @@ struct DeviceLayout {
     // ~(element index) into the frame's global copy (Lg for lidx, Eg for vpos).
     size_t cband_lidx = 0; // int32 [(wc-1)*n]
     size_t cband_vpos = 0; // int32 [n*(wc-1)]
+    // Exchange cluster view (spa_cluster.cu; C = xband_cluster_size CTAs per
+    // frame exchange message segments with bulk DSMEM copies).  Slots are byte
+    // offsets into the owning CTA's message buffer (see spa_cluster.cu):
+    size_t xband_ridx = 0; // uint16 [(wc-1)*n]  band edge (b>=1, p) -> slot in its row owner's buffer
+    size_t xband_sidx = 0; // uint16 [n*(wc-1)]  variable v, band b>=1 -> slot in its variable owner's buffer
+    size_t xband_seg = 0;  // int32 [3][C][C]    send offset, receive offset, bytes of segment (var owner, row owner)
     size_t total = 0;
 };
 
@@ -60,6 +66,11 @@ struct DeviceCode {
     int32_t cluster;               // C of the cluster band view (0: none)
     const int32_t *cband_lidx;
     const int32_t *cband_vpos;
+    int32_t xcluster;              // C of the exchange cluster view (0: none)
+    int32_t xcap;                  // message buffer capacity per CTA (floats, multiple of 4)
+    const uint16_t *xband_ridx;
+    const uint16_t *xband_sidx;
+    const int32_t *xband_seg;
 };
 
 // Cluster size for the cluster band kernel: the smallest power of two C <= 16
@@ -70,6 +81,22 @@ inline int band_cluster_size(int32_t n, int32_t wc, int32_t wr) {
     if (one + 1024 <= 227 * 1024) return 0;
     for (int C = 2; C <= 16; C *= 2)
         if ((n / wr) % C == 0 && one / C <= 200 * 1024) return C;
+    return 0;
+}
+
+// Cluster size of the exchange cluster kernel (spa_cluster.cu): the smallest
+// power of two C <= 16 with mb % C == 0 whose three message buffers of
+// xband_capacity floats fit one CTA's shared memory and whose slots fit 16-bit
+// byte offsets; 0 when a frame fits one SM or no such C exists.
+inline int32_t xband_capacity(int32_t n, int32_t wc, int32_t C) { return ((wc - 1) * (n / C) + 4 * C + 3) & ~3; }
+inline int xband_cluster_size(int32_t n, int32_t wc, int32_t wr) {
+    if (wc < 2 || wr < 1 || n % wr) return 0;
+    if (size_t(wc) * size_t(n) * 4 + 1024 <= 227 * 1024) return 0;
+    for (int C = 2; C <= 16; C *= 2) {
+        if ((n / wr) % C) continue;
+        const size_t cap = size_t(xband_capacity(n, wc, C));
+        if (cap * 4 <= 65532 && 3 * cap * 4 + 1024 <= 227 * 1024) return C;
+    }
     return 0;
 }
 
@@ -102,6 +129,8 @@ struct ldpc_code {
 
 namespace ldpc {
 DeviceLayout compute_layout(const ldpc_code &c, bool with_G);
+void xband_tables(const ldpc_code &c, int C, std::vector<uint16_t> &ridx, std::vector<uint16_t> &sidx,
+                  std::vector<int32_t> &seg);
 
 // Launch plan of the Gallager band kernel (spa_band.cu).
 struct BandPlan {
@@ -133,6 +162,22 @@ struct ClusterPlan {
     size_t ws_bytes = 0;
 };
 bool cluster_plan(const ldpc_code &c, int64_t frames, bool et, ClusterPlan &p);
+
+// Launch plan of the exchange cluster kernel (spa_cluster.cu; variant 7).
+struct XClusterPlan {
+    void *kernel = nullptr;
+    int cluster = 0;
+    int threads = 0;
+    int grid = 0;
+    size_t smem = 0;
+    size_t ws_bytes = 0;
+};
+// false unless the bound code has an exchange cluster view, fixed iterations
+// and an instantiated (wc, wr, rows-per-thread, C).
+bool xcluster_plan(const ldpc_code &c, int64_t frames, bool et, XClusterPlan &p);
+ldpc_status xcluster_launch(const ldpc_code &c, const XClusterPlan &p, const float *llr, int64_t frames,
+                            const ldpc_decode_opts &o, uint32_t *bits, uint8_t *syn, int32_t *iters, float *post,
+                            void *stream);
 ldpc_status cluster_launch(const ldpc_code &c, const ClusterPlan &p, const float *llr, int64_t frames,
                            const ldpc_decode_opts &o, uint32_t *bits, uint8_t *syn, int32_t *iters, float *post,
                            void *ws, size_t ws_bytes, void *stream);

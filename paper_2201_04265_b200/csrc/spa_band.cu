@@ -25,193 +25,12 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "band_common.cuh"
 #include "ldpc_internal.h"
 
 namespace ldpc {
 namespace {
-
-constexpr float kL2E = 1.44269504088896341f;
-constexpr float kLn2 = 0.693147180559945309f;
-constexpr float kClampB = 43.2808512f;    // 30 log2(e)            (reading Q7)
-constexpr float kEMaxB = 40.86313714f;    // log2(2e12 - 1) = E_MAX log2(e)
-// psi(y) = log2(e) phi(y ln2), y >= 0:
-//   y <= 1.8033688: psi = C1 - lg2(y) + y^2 q(y^2)     (one lg2)
-//   y >  1.8033688: psi = t h(t^2),  t = 2^-y          (one ex2)
-constexpr float kSplitB = 1.8033688f;
-constexpr float kUltraLargeB = 10.0f;           // psi(y) = h0 2^-y within 3.2e-7 relative
-constexpr float kUltraSmallB = 0.0009765625f;   // psi(y) = C1 - lg2(y) within 5e-9 relative
-constexpr float kC1 = 1.528766373f;
-constexpr float kQ0 = 0.0577617388f, kQ1 = -0.00161740689f, kQ2 = 5.33304814e-05f, kQ3 = -1.50169545e-06f;
-constexpr float kH0 = 2.88539008f, kH1 = 0.961820197f, kH2 = 0.574983425f, kH3 = 0.461572595f;
-
-__device__ __forceinline__ float ex2a(float x) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-__device__ __forceinline__ float lg2a(float x) {
-    float y;
-    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
-__device__ __forceinline__ float psi(float y) {
-    const float s = y * y;
-    const float q = fmaf(fmaf(fmaf(kQ3, s, kQ2), s, kQ1), s, kQ0);
-    const float small = fmaf(s, q, kC1) - lg2a(y);
-    const float t = ex2a(-y);
-    const float u = t * t;
-    const float h = fmaf(fmaf(fmaf(kH3, u, kH2), u, kH1), u, kH0);
-    const float large = t * h;
-    return y > kSplitB ? large : small;
-}
-__device__ __forceinline__ float psi_small(float y) {
-    const float s = y * y;
-    const float q = fmaf(fmaf(fmaf(kQ3, s, kQ2), s, kQ1), s, kQ0);
-    return fmaf(s, q, kC1) - lg2a(y);
-}
-__device__ __forceinline__ float psi_large(float y) {
-    const float t = ex2a(-y);
-    const float u = t * t;
-    return t * fmaf(fmaf(fmaf(kH3, u, kH2), u, kH1), u, kH0);
-}
-
-// psi over a row.  When every input of every active lane of the warp falls in
-// one regime -- the common case once a frame has converged: |L_vc| large
-// (first psi), exclusive sums tiny (second psi) -- only that regime is
-// evaluated (one SFU op and 5 FMA-pipe ops instead of two and 11).
-// LARGE_FIRST orders the two warp votes by the expected regime.  VOTE is off
-// under early termination: a frame stops as soon as it converges, so the
-// uniform regime never lasts and the votes would be pure overhead.
-template <int D, bool LARGE_FIRST, bool VOTE>
-__device__ __forceinline__ void psi_row(const float (&in)[D], float (&out)[D]) {
-    if (!VOTE) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) out[j] = psi(in[j]);
-        return;
-    }
-    const unsigned act = __activemask();
-    float lo = in[0], hi = in[0];
-#pragma unroll
-    for (int j = 1; j < D; ++j) {
-        if (LARGE_FIRST) lo = fminf(lo, in[j]);
-        else hi = fmaxf(hi, in[j]);
-    }
-    // Deep-converged tiers: y >= 10 -> psi = h0 2^-y (dropped terms <= 3.2e-7
-    // relative); y <= 2^-10 -> psi = C1 - lg2 y (dropped term <= 5.5e-8 against
-    // psi >= 11.5).  One SFU op and one FMA-pipe op per input.
-    if (LARGE_FIRST ? __all_sync(act, lo >= kUltraLargeB) : __all_sync(act, hi <= kUltraSmallB)) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) out[j] = LARGE_FIRST ? kH0 * ex2a(-in[j]) : kC1 - lg2a(in[j]);
-        return;
-    }
-    if (LARGE_FIRST ? __all_sync(act, lo > kSplitB) : __all_sync(act, hi <= kSplitB)) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) out[j] = LARGE_FIRST ? psi_large(in[j]) : psi_small(in[j]);
-        return;
-    }
-#pragma unroll
-    for (int j = 1; j < D; ++j) {
-        if (LARGE_FIRST) hi = fmaxf(hi, in[j]);
-        else lo = fminf(lo, in[j]);
-    }
-    if (LARGE_FIRST ? __all_sync(act, hi <= kSplitB) : __all_sync(act, lo > kSplitB)) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) out[j] = LARGE_FIRST ? psi_small(in[j]) : psi_large(in[j]);
-        return;
-    }
-#pragma unroll
-    for (int j = 0; j < D; ++j) out[j] = psi(in[j]);
-}
-
-// Check-node update of one row (Eq. 5, readings Q2/Q3/Q7) in log2 units.
-// x[j] = L'_v - E'_cv (not yet clamped); e[j] <- new E'_cv.
-template <int D, bool VOTE>
-__device__ __forceinline__ void check_row(const float (&x)[D], float (&e)[D]) {
-    float f[D], ax[D];
-    uint32_t sx = (D & 1) ? 0x80000000u : 0u;     // (-1)^{d_c}
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-        sx ^= __float_as_uint(x[j]);
-        ax[j] = fminf(fabsf(x[j]), kClampB);
-    }
-    psi_row<D, true, VOTE>(ax, f);
-    float ex[D];
-    float acc = 0.0f;
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-        ex[j] = acc;
-        acc += f[j];
-    }
-    acc = 0.0f;
-#pragma unroll
-    for (int j = D - 1; j >= 0; --j) {
-        ex[j] += acc;
-        acc += f[j];
-    }
-    float g[D];
-    psi_row<D, false, VOTE>(ex, g);
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-        const float mag = fminf(g[j], kEMaxB);
-        const uint32_t sgn = (sx ^ __float_as_uint(x[j])) & 0x80000000u;
-        e[j] = __uint_as_float(__float_as_uint(mag) | sgn);
-    }
-}
-
-template <int D>
-__device__ __forceinline__ void lds_row(const char *smem, uint32_t byte_off, float (&o)[D]) {
-    const float *p = reinterpret_cast<const float *>(smem + byte_off);
-    if constexpr (D % 4 == 0) {
-#pragma unroll
-        for (int j = 0; j < D; j += 4) {
-            float4 t = *reinterpret_cast<const float4 *>(p + j);
-            o[j] = t.x; o[j + 1] = t.y; o[j + 2] = t.z; o[j + 3] = t.w;
-        }
-    } else if constexpr (D % 2 == 0) {
-#pragma unroll
-        for (int j = 0; j < D; j += 2) {
-            float2 t = *reinterpret_cast<const float2 *>(p + j);
-            o[j] = t.x; o[j + 1] = t.y;
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < D; ++j) o[j] = p[j];
-    }
-}
-template <int D>
-__device__ __forceinline__ void sts_row(char *smem, uint32_t byte_off, const float (&o)[D]) {
-    float *p = reinterpret_cast<float *>(smem + byte_off);
-    if constexpr (D % 4 == 0) {
-#pragma unroll
-        for (int j = 0; j < D; j += 4) *reinterpret_cast<float4 *>(p + j) = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
-    } else if constexpr (D % 2 == 0) {
-#pragma unroll
-        for (int j = 0; j < D; j += 2) *reinterpret_cast<float2 *>(p + j) = make_float2(o[j], o[j + 1]);
-    } else {
-#pragma unroll
-        for (int j = 0; j < D; ++j) p[j] = o[j];
-    }
-}
-template <int D>
-__device__ __forceinline__ void ldg_idx(const int32_t *p, int32_t (&o)[D]) {
-    if constexpr (D % 4 == 0) {
-#pragma unroll
-        for (int j = 0; j < D; j += 4) {
-            int4 t = __ldg(reinterpret_cast<const int4 *>(p + j));
-            o[j] = t.x; o[j + 1] = t.y; o[j + 2] = t.z; o[j + 3] = t.w;
-        }
-    } else if constexpr (D % 2 == 0) {
-#pragma unroll
-        for (int j = 0; j < D; j += 2) {
-            int2 t = __ldg(reinterpret_cast<const int2 *>(p + j));
-            o[j] = t.x; o[j + 1] = t.y;
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < D; ++j) o[j] = __ldg(p + j);
-    }
-}
+using namespace band;
 
 struct BandArgs {
     DeviceCode code;
@@ -290,11 +109,13 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
                 if (tt < S && r < mb) {
                     float lv[WR], x[WR];
                     lds_row<WR>(smem, lbase + uint32_t(r) * WR * 4u, lv);
+                    uint32_t rp = 0;      // this row's syndrome bit (Eq. 1)
 #pragma unroll
                     for (int j = 0; j < WR; ++j) {
                         x[j] = lv[j] - e0[k][j];
-                        if (ET) synd ^= (lv[j] >= 0.0f) ? 1u : 0u;
+                        if (ET) rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
                     }
+                    synd |= rp;
                     check_row<WR, !ET>(x, e0[k]);
                 }
             }
@@ -324,12 +145,14 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
                     } else {
                         lds_row<WR>(smem, uint32_t(r) * WR * 4u, e);
                     }
+                    uint32_t rp = 0;
 #pragma unroll
                     for (int j = 0; j < WR; ++j) {
                         const float lv = *reinterpret_cast<const float *>(smem + li[j]);
                         x[j] = lv - e[j];
-                        if (ET) synd ^= (lv >= 0.0f) ? 1u : 0u;
+                        if (ET) rp ^= (lv >= 0.0f) ? 1u : 0u;
                     }
+                    synd |= rp;
                     check_row<WR, !ET>(x, e);
                     if (VM) {
 #pragma unroll
@@ -387,11 +210,17 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
         bool ok = stopped;
         if (!stopped) {
             uint32_t synd = 0;
-            for (int r = tt; r < mb; r += T)
-                for (int j = 0; j < WR; ++j) synd ^= (Ls[r * WR + j] >= 0.0f) ? 1u : 0u;
-            for (int r = tt; r < NB * mb; r += T)
+            for (int r = tt; r < mb; r += T) {
+                uint32_t rp = 0;
+                for (int j = 0; j < WR; ++j) rp ^= (Ls[r * WR + j] >= 0.0f) ? 1u : 0u;
+                synd |= rp;
+            }
+            for (int r = tt; r < NB * mb; r += T) {
+                uint32_t rp = 0;
                 for (int j = 0; j < WR; ++j)
-                    synd ^= (*reinterpret_cast<const float *>(smem + __ldg(lidx + size_t(r) * WR + j)) >= 0.0f) ? 1u : 0u;
+                    rp ^= (*reinterpret_cast<const float *>(smem + __ldg(lidx + size_t(r) * WR + j)) >= 0.0f) ? 1u : 0u;
+                synd |= rp;
+            }
             ok = !cta_sync_or(synd != 0);
         }
         // ---- a6/a8: hard decisions (Eq. 8) packed by ballot, flags, posteriors
@@ -591,12 +420,17 @@ __global__ void __launch_bounds__(1024, 1) band_cluster_kernel(const ClusterArgs
         }
         // syndrome of z = [L >= 0] over own rows, OR-ed across the cluster
         uint32_t synd = 0;
-        for (int r = tt; r < mbq; r += T)
-            for (int j = 0; j < WR; ++j) synd ^= (Ls[r * WR + j] >= 0.0f) ? 1u : 0u;
+        for (int r = tt; r < mbq; r += T) {
+            uint32_t rp = 0;
+            for (int j = 0; j < WR; ++j) rp ^= (Ls[r * WR + j] >= 0.0f) ? 1u : 0u;
+            synd |= rp;
+        }
         for (int r = tt; r < NB * mbq; r += T) {
             const int b = r / mbq, lr = r - b * mbq;
             const int64_t gpos = int64_t(b) * n + int64_t(q * mbq + lr) * WR;
-            for (int j = 0; j < WR; ++j) synd ^= (ld_l_or_g(smem, Lg, __ldg(lidx + gpos + j)) >= 0.0f) ? 1u : 0u;
+            uint32_t rp = 0;
+            for (int j = 0; j < WR; ++j) rp ^= (ld_l_or_g(smem, Lg, __ldg(lidx + gpos + j)) >= 0.0f) ? 1u : 0u;
+            synd |= rp;
         }
         const int any = __syncthreads_or(synd != 0);
         if (tt == 0) flags[q] = any;

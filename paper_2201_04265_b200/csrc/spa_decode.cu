@@ -487,6 +487,14 @@ ldpc_status ldpc_decode_variant(const ldpc_code *code, int64_t frames, const ldp
         }
         if (opts->variant != 0) return LDPC_ERR_UNSUPPORTED;
     }
+    if (opts->variant == 0 || opts->variant == 7) {
+        ldpc::XClusterPlan xp;
+        if (ldpc::xcluster_plan(*code, frames, opts->early_term != 0, xp)) {
+            *variant = 7;
+            return LDPC_OK;
+        }
+        if (opts->variant == 7) return LDPC_ERR_UNSUPPORTED;
+    }
     if (opts->variant == 0 || opts->variant == 5) {
         ldpc::ClusterPlan cp;
         if (ldpc::cluster_plan(*code, frames, opts->early_term != 0, cp)) {
@@ -512,6 +520,14 @@ ldpc_status ldpc_decode_workspace_bytes(const ldpc_code *code, int64_t frames, c
             return LDPC_OK;
         }
         if (opts->variant != 0) return LDPC_ERR_UNSUPPORTED;
+    }
+    if (opts->variant == 0 || opts->variant == 7) {
+        ldpc::XClusterPlan xp;
+        if (ldpc::xcluster_plan(*code, std::max<int64_t>(frames, 1), opts->early_term != 0, xp)) {
+            *bytes = xp.ws_bytes;
+            return LDPC_OK;
+        }
+        if (opts->variant == 7) return LDPC_ERR_UNSUPPORTED;
     }
     if (opts->variant == 0 || opts->variant == 5) {
         ldpc::ClusterPlan cp;
@@ -543,6 +559,13 @@ ldpc_status ldpc_decode(const ldpc_code *code, const float *d_llr, int64_t frame
             return ldpc::band_launch(*code, bp, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters, d_posterior,
                                      d_ws, ws_bytes, stream);
         if (opts->variant != 0) return LDPC_ERR_UNSUPPORTED;
+    }
+    if (opts->variant == 0 || opts->variant == 7) {
+        ldpc::XClusterPlan xp;
+        if (ldpc::xcluster_plan(*code, frames, opts->early_term != 0, xp))
+            return ldpc::xcluster_launch(*code, xp, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters,
+                                         d_posterior, stream);
+        if (opts->variant == 7) return LDPC_ERR_UNSUPPORTED;
     }
     if (opts->variant == 0 || opts->variant == 5) {
         ldpc::ClusterPlan cp;
