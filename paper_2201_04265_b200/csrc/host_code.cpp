@@ -95,7 +95,8 @@ DeviceLayout compute_layout(const ldpc_code &c, bool with_G) {
         if (const int C = xband_cluster_size(c.n, c.wc, c.wr)) {
             L.xband_ridx = off; off = align256(off + sizeof(uint16_t) * nb);
             L.xband_sidx = off; off = align256(off + sizeof(uint16_t) * nb);
-            L.xband_seg = off;  off = align256(off + sizeof(int32_t) * 3 * size_t(C) * size_t(C));
+            const size_t H = size_t(xband_rows_per_thread(c.n / c.wr / C));
+            L.xband_seg = off;  off = align256(off + sizeof(int32_t) * 3 * size_t(C) * size_t(C) * H * size_t(c.wc - 1));
         }
     }
     if (with_G) {
@@ -111,47 +112,62 @@ DeviceLayout compute_layout(const ldpc_code &c, bool with_G) {
 
 // Message-segment tables of the exchange cluster kernel (spa_cluster.cu).
 // CTA q owns band rows [q mbq, (q+1) mbq) of every band and the variables
-// [q nq, (q+1) nq) of its band-0 rows.  Every band-b >= 1 edge (b, p) joins
-// row owner d = (p / wr) / mbq and variable owner s = pi_b[p] / nq.  Its two
-// messages per iteration travel in segment (s, d): L_vc from s to d, E_cv
-// back from d to s, at the same rank r inside the segment (segments hold
-// their edges in ascending (b, p)).  A CTA's buffer laid out by destination
-// ("send layout", its variables' edges) puts segment (s, d) at sOff[s][d]; laid
-// out by source ("receive layout", its rows' edges) puts it at rOff[s][d].
-// Segments are padded to 16 bytes (bulk-copy granularity).
-//   ridx[(b-1) n + p]    = rOff[s][d] + 4 r   (byte slot in d's buffer)
-//   sidx[v (wc-1) + b-1] = sOff[s][d] + 4 r   (byte slot in s's buffer)
-//   seg = { sOff, rOff, bytes } as three C x C int32 arrays indexed [s][d].
+// [q nq, (q+1) nq) of its band-0 rows; its local band-0 row rl is processed in
+// V-phase chunk h = rl / T (T = xband_threads(mbq)).  Every band-b >= 1 edge
+// (b, p) joins variable owner s = pi_b[p] / nq (chunk h of its variable) and
+// row owner d = (p / wr) / mbq.  The edge has ONE slot in s's VAR region
+// (E_cv arrives there, L_vc is written over it) and ONE slot in d's ROW region
+// (L_vc arrives there, E_cv is written over it).  Edges sharing (s, d, h, b)
+// form a segment, contiguous and in ascending p in both regions:
+//   var region of s: segments ordered by (h, b, d)   -- V-phase chunk h ships
+//                                                      its NB C segments at once
+//   row region of d: segments ordered by (b, s, h)   -- C-phase band b ships
+//                                                      its C H segments at once
+// Segments are padded to 16 bytes (bulk-copy granularity).  Outputs:
+//   ridx[(b-1) n + p]    = byte slot of edge (b, p) in d's row region
+//   sidx[v (wc-1) + b-1] = byte slot of edge (b, pi_b^-1(v)) in s's var region
+//   seg = { varOff, rowOff, bytes }, three int32 arrays indexed by
+//         key(s, d, h, b) = ((s C + d) H + h) (wc-1) + (b-1).
 void xband_tables(const ldpc_code &c, int C, std::vector<uint16_t> &ridx, std::vector<uint16_t> &sidx,
                   std::vector<int32_t> &seg) {
-    const int32_t n = c.n, wc = c.wc, wr = c.wr, mbq = n / wr / C, nq = n / C;
-    const size_t nb = size_t(wc - 1) * size_t(n);
-    std::vector<int32_t> cnt(size_t(C) * C, 0), rank(nb);
-    for (int32_t b = 1; b < wc; ++b)
+    const int32_t n = c.n, wc = c.wc, wr = c.wr, NB = wc - 1, mbq = n / wr / C, nq = mbq * wr;
+    const int32_t T = xband_threads(mbq), H = xband_rows_per_thread(mbq);
+    const size_t nb = size_t(NB) * size_t(n), nkey = size_t(C) * C * H * NB;
+    auto key = [&](int32_t s, int32_t d, int32_t h, int32_t b) { return ((size_t(s) * C + d) * H + h) * NB + b; };
+    std::vector<int32_t> cnt(nkey, 0), rank(nb), kof(nb);
+    for (int32_t b = 0; b < NB; ++b)
         for (int32_t p = 0; p < n; ++p) {
-            const int32_t d = (p / wr) / mbq, s = c.col_idx[size_t(b) * n + p] / nq;
-            rank[size_t(b - 1) * n + p] = cnt[size_t(s) * C + d]++;
+            const int32_t v = c.col_idx[size_t(b + 1) * n + p];
+            const int32_t s = v / nq, d = (p / wr) / mbq, h = ((v - s * nq) / wr) / T;
+            const size_t k = key(s, d, h, b);
+            kof[size_t(b) * n + p] = int32_t(k);
+            rank[size_t(b) * n + p] = cnt[k]++;
         }
     auto pad = [](int32_t x) { return (x + 3) & ~3; };
-    seg.assign(3 * size_t(C) * C, 0);
-    int32_t *sOff = seg.data(), *rOff = seg.data() + C * C, *bytes = seg.data() + 2 * C * C;
+    seg.assign(3 * nkey, 0);
+    int32_t *varOff = seg.data(), *rowOff = seg.data() + nkey, *bytes = seg.data() + 2 * nkey;
     for (int32_t s = 0; s < C; ++s) {
         int32_t o = 0;
-        for (int32_t d = 0; d < C; ++d) { sOff[s * C + d] = 4 * o; o += pad(cnt[size_t(s) * C + d]); }
+        for (int32_t h = 0; h < H; ++h)
+            for (int32_t b = 0; b < NB; ++b)
+                for (int32_t d = 0; d < C; ++d) { varOff[key(s, d, h, b)] = 4 * o; o += pad(cnt[key(s, d, h, b)]); }
     }
     for (int32_t d = 0; d < C; ++d) {
         int32_t o = 0;
-        for (int32_t s = 0; s < C; ++s) { rOff[s * C + d] = 4 * o; o += pad(cnt[size_t(s) * C + d]); }
+        for (int32_t b = 0; b < NB; ++b)
+            for (int32_t s = 0; s < C; ++s)
+                for (int32_t h = 0; h < H; ++h) { rowOff[key(s, d, h, b)] = 4 * o; o += pad(cnt[key(s, d, h, b)]); }
     }
-    for (int32_t i = 0; i < C * C; ++i) bytes[i] = 4 * pad(cnt[i]);
+    for (size_t i = 0; i < nkey; ++i) bytes[i] = 4 * pad(cnt[i]);
     ridx.assign(nb, 0);
     sidx.assign(nb, 0);
-    for (int32_t b = 1; b < wc; ++b)
+    for (int32_t b = 0; b < NB; ++b)
         for (int32_t p = 0; p < n; ++p) {
-            const int32_t v = c.col_idx[size_t(b) * n + p];
-            const int32_t d = (p / wr) / mbq, s = v / nq, r = rank[size_t(b - 1) * n + p];
-            ridx[size_t(b - 1) * n + p] = uint16_t(rOff[s * C + d] + 4 * r);
-            sidx[size_t(v) * (wc - 1) + (b - 1)] = uint16_t(sOff[s * C + d] + 4 * r);
+            const int32_t v = c.col_idx[size_t(b + 1) * n + p];
+            const size_t k = size_t(kof[size_t(b) * n + p]);
+            const int32_t r = rank[size_t(b) * n + p];
+            ridx[size_t(b) * n + p] = uint16_t(rowOff[k] + 4 * r);
+            sidx[size_t(v) * NB + b] = uint16_t(varOff[k] + 4 * r);
         }
 }
 }  // namespace ldpc
@@ -490,7 +506,7 @@ ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, vo
     D.cband_lidx = D.cluster ? reinterpret_cast<const int32_t *>(base + L.cband_lidx) : nullptr;
     D.cband_vpos = D.cluster ? reinterpret_cast<const int32_t *>(base + L.cband_vpos) : nullptr;
     D.xcluster = (code->gallager && code->wc >= 2) ? ldpc::xband_cluster_size(code->n, code->wc, code->wr) : 0;
-    D.xcap = D.xcluster ? ldpc::xband_capacity(code->n, code->wc, D.xcluster) : 0;
+    D.xcap = D.xcluster ? ldpc::xband_capacity(code->n, code->wc, code->wr, D.xcluster) : 0;
     D.xband_ridx = D.xcluster ? reinterpret_cast<const uint16_t *>(base + L.xband_ridx) : nullptr;
     D.xband_sidx = D.xcluster ? reinterpret_cast<const uint16_t *>(base + L.xband_sidx) : nullptr;
     D.xband_seg = D.xcluster ? reinterpret_cast<const int32_t *>(base + L.xband_seg) : nullptr;

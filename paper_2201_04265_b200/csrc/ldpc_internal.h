@@ -40,7 +40,7 @@ struct DeviceLayout {
     // offsets into the owning CTA's message buffer (see spa_cluster.cu):
     size_t xband_ridx = 0; // uint16 [(wc-1)*n]  band edge (b>=1, p) -> slot in its row owner's buffer
     size_t xband_sidx = 0; // uint16 [n*(wc-1)]  variable v, band b>=1 -> slot in its variable owner's buffer
-    size_t xband_seg = 0;  // int32 [3][C][C]    send offset, receive offset, bytes of segment (var owner, row owner)
+    size_t xband_seg = 0;  // int32 [3][C C H (wc-1)] var-region offset, row-region offset, bytes per segment
     size_t total = 0;
 };
 
@@ -67,7 +67,7 @@ struct DeviceCode {
     const int32_t *cband_lidx;
     const int32_t *cband_vpos;
     int32_t xcluster;              // C of the exchange cluster view (0: none)
-    int32_t xcap;                  // message buffer capacity per CTA (floats, multiple of 4)
+    int32_t xcap;                  // message region capacity (floats, multiple of 4)
     const uint16_t *xband_ridx;
     const uint16_t *xband_sidx;
     const int32_t *xband_seg;
@@ -84,18 +84,41 @@ inline int band_cluster_size(int32_t n, int32_t wc, int32_t wr) {
     return 0;
 }
 
-// Cluster size of the exchange cluster kernel (spa_cluster.cu): the smallest
-// power of two C <= 16 with mb % C == 0 whose three message buffers of
-// xband_capacity floats fit one CTA's shared memory and whose slots fit 16-bit
-// byte offsets; 0 when a frame fits one SM or no such C exists.
-inline int32_t xband_capacity(int32_t n, int32_t wc, int32_t C) { return ((wc - 1) * (n / C) + 4 * C + 3) & ~3; }
+// Exchange cluster kernel (spa_cluster.cu): C CTAs per frame, CTA q owns
+// mbq = n / wr / C rows of every band and the nq = mbq wr variables of its
+// band-0 rows.  Threads and rows per thread (= V-phase chunks H) of a CTA:
+inline int xband_rows_per_thread(int32_t mbq) {
+    const int b0 = mbq > 0 ? (mbq + 1023) / 1024 : 1;
+    return b0 == 3 ? 4 : b0;                      // instantiated: 1, 2, 4
+}
+inline int xband_threads(int32_t mbq) {
+    const int b0 = xband_rows_per_thread(mbq);
+    return ((mbq + b0 - 1) / b0 + 31) / 32 * 32;
+}
+// Capacity (floats) of one message region: (wc-1) nq edge slots plus up to 3
+// floats of 16-byte padding per segment (H chunks x (wc-1) bands x C peers).
+inline int32_t xband_capacity(int32_t n, int32_t wc, int32_t wr, int32_t C) {
+    const int32_t mbq = n / wr / C, nq = mbq * wr;
+    const int32_t H = xband_rows_per_thread(mbq);
+    return ((wc - 1) * nq + 3 * H * (wc - 1) * C + 3) & ~3;
+}
+// Shared memory of the kernel: two regions + the CTA's two 16-bit slot tables
+// + barriers and flags.
+inline size_t xband_smem_bytes(int32_t n, int32_t wc, int32_t wr, int32_t C) {
+    const size_t nq = size_t(n / wr / C) * size_t(wr);
+    return 2 * size_t(xband_capacity(n, wc, wr, C)) * 4 + 2 * size_t(wc - 1) * nq * 2 + 32 + 4 * size_t(C);
+}
+// The smallest power of two C <= 16 with mb % C == 0 whose shared memory fits
+// one CTA and whose region offsets fit 16 bits; 0 when a frame fits one SM or
+// no such C exists.
 inline int xband_cluster_size(int32_t n, int32_t wc, int32_t wr) {
     if (wc < 2 || wr < 1 || n % wr) return 0;
     if (size_t(wc) * size_t(n) * 4 + 1024 <= 227 * 1024) return 0;
     for (int C = 2; C <= 16; C *= 2) {
         if ((n / wr) % C) continue;
-        const size_t cap = size_t(xband_capacity(n, wc, C));
-        if (cap * 4 <= 65532 && 3 * cap * 4 + 1024 <= 227 * 1024) return C;
+        if (size_t(xband_capacity(n, wc, wr, C)) * 4 > 65532) continue;
+        if (xband_threads(n / wr / C) > 1024) continue;
+        if (xband_smem_bytes(n, wc, wr, C) + 1024 <= 227 * 1024) return C;
     }
     return 0;
 }

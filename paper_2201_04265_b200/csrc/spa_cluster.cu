@@ -10,30 +10,29 @@
 //     (band 0 is contiguous): their E lives in registers and the
 //     variable update (Eq. 6/7) and band-0 check update run thread-locally;
 //   * band-b >= 1 rows [q mbq, (q+1) mbq) (check-node update, Eq. 5).
-// Each half-iteration, every CTA writes the messages it produces into a local
-// SEND buffer laid out by destination CTA (random local shared-memory stores
-// at precomputed 16-bit slots), then C threads each push one contiguous
-// segment to one destination CTA with cp.async.bulk shared::cta ->
-// shared::cluster, completing on the destination's mbarrier (complete_tx).
-// Random remote 4-byte DSMEM accesses run at ~0.4/clk/SM
-// (profiles/r01_microbench.txt); the segment exchange turns them into local
-// random accesses plus bulk transfers.
+// Message state lives IN PLACE in two shared-memory regions per CTA: every
+// band-b >= 1 edge has one slot in its variable owner's VAR region and one in
+// its row owner's ROW region (host_code.cpp xband_tables).
+//   C-phase: read L_vc from the ROW slot, write E_cv over it; after each band,
+//            ship that band's segments (one per (variable owner, V chunk)) to
+//            the owners' VAR regions.
+//   V-phase: read E_cv from the VAR slots, write L_vc over them; after each
+//            row chunk h, ship its segments (one per (band, row owner)) to the
+//            owners' ROW regions.
+// Shipping = cp.async.bulk shared::cta -> shared::cluster, complete_tx on the
+// receiver's region barrier; early chunks travel while later chunks compute.
+// Random remote 4-byte DSMEM accesses run at ~0.4/clk/SM and bulk segment
+// exchange at ~12 B/clk/SM (profiles/r01_microbench*.txt), hence the segments
+// and the overlap.  The two slot tables of the CTA are copied to shared memory
+// once per launch.
 //
-// Buffers (floats, per CTA): SEND[cap], RECV[2][cap] (double-buffered by
-// exchange parity).  Exchange h carries L_vc (variable -> check) or E_cv
-// (check -> variable); one edge uses the same slot for both directions, so a
-// phase reads RECV at slot s and writes SEND at the same slot s.
-// Synchronisation per exchange h (x = h & 1):
-//   1. writers: fence.proxy.async; __syncthreads
-//   2. thread d < C: bulk copy of segment (q -> d) into d's RECV[x],
-//      complete_tx on d's recv_bar[x]
-//   3. all: wait recv_bar[x] (phase h >> 1)
-//   4. thread 0 re-arms recv_bar[x] (expect_tx of exchange h + 2);
-//      thread s < C arrives on CTA s's free_bar (its segment to us landed)
-//   5. the next phase waits free_bar (exchange h) before writing SEND.
-// A remote RECV[x] is free when we write it at exchange h + 2: that needs
-// free_bar(h + 1) of ours, i.e. every destination passed step 1 of exchange
-// h + 1, i.e. finished reading RECV[x] in its phase.
+// Why no region is overwritten while still needed: a CTA writes its VAR
+// region only after its VAR barrier completed (every row owner shipped every
+// band, i.e. finished its C-phase), and its outgoing copies from that region
+// (previous V-phase) were complete before any row owner could start the
+// C-phase whose results just arrived; the ROW region symmetrically.  A CTA
+// ships into a peer's region only after having received that peer's whole
+// previous exchange, which the peer issues after its last read of the region.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -136,143 +135,163 @@ struct XArgs {
     float *posterior;
 };
 
-// Shared memory: SEND | RECV0 | RECV1 (cap floats each) | recv_bar[2] | free_bar | flags[C]
-template <int WR, int WC, int B0, int C>
+// Shared memory: VAR region | ROW region (cap floats each) | var slot table
+// u16 [nq][NB] | row slot table u16 [NB][mbq][WR] | var_bar, row_bar | flags[C]
+template <int WR, int WC, int H, int C>
 __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
     extern __shared__ __align__(128) char smem[];
     constexpr int NB = WC - 1;
-    constexpr int B1 = NB * B0;
     const DeviceCode &code = a.code;
     const int n = code.n, mb = code.mb, mbq = mb / C, nq = n / C;
     const int T = blockDim.x, tt = threadIdx.x;
     const uint32_t cap_b = uint32_t(code.xcap) * 4u;
     const uint32_t q = cluster_ctarank();
     const int64_t cid = cluster_id_x(), ncl = ncluster_x();
-    char *send = smem;
-    char *recv0 = smem + cap_b;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + 3 * cap_b);
-    int *flags = reinterpret_cast<int *>(bars + 4);
-    const uint32_t send_s = saddr(send), recv_s = saddr(recv0), bar_s = saddr(bars);
-    const uint32_t free_s = bar_s + 16;
-    const int32_t *sOff = code.xband_seg, *rOff = code.xband_seg + C * C, *sbytes = code.xband_seg + 2 * C * C;
+    char *varr = smem;
+    char *rowr = smem + cap_b;
+    uint16_t *vtab = reinterpret_cast<uint16_t *>(smem + 2 * cap_b);
+    uint16_t *rtab = vtab + size_t(nq) * NB;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + ((2 * cap_b + 4u * uint32_t(NB * nq) + 15u) & ~15u));
+    int *flags = reinterpret_cast<int *>(bars + 2);
+    const uint32_t var_s = saddr(varr), row_s = saddr(rowr), vbar = saddr(bars), rbar = vbar + 8;
+    const int nkey = C * C * H * NB;
+    const int32_t *varOff = code.xband_seg, *rowOff = code.xband_seg + nkey, *sbytes = code.xband_seg + 2 * nkey;
+    auto key = [](int s, int d, int h, int b) { return ((s * C + d) * H + h) * NB + b; };
 
-    // bytes CTA q receives in an L exchange (from every variable owner s) and
-    // in an E exchange (from every row owner d)
-    uint32_t rx_l = 0, rx_e = 0;
-#pragma unroll
-    for (int s = 0; s < C; ++s) {
-        rx_l += uint32_t(__ldg(sbytes + s * C + q));
-        rx_e += uint32_t(__ldg(sbytes + q * C + s));
+    // slot tables of CTA q -> shared memory (once)
+    {
+        const uint32_t *src = reinterpret_cast<const uint32_t *>(code.xband_sidx + size_t(q) * nq * NB);
+        uint32_t *dst = reinterpret_cast<uint32_t *>(vtab);
+        for (int i = tt; i < nq * NB / 2; i += T) dst[i] = __ldg(src + i);
+        for (int b = 0; b < NB; ++b) {
+            const uint32_t *rs = reinterpret_cast<const uint32_t *>(code.xband_ridx + size_t(b) * n + size_t(q) * mbq * WR);
+            uint32_t *rd = reinterpret_cast<uint32_t *>(rtab + size_t(b) * mbq * WR);
+            for (int i = tt; i < mbq * WR / 2; i += T) rd[i] = __ldg(rs + i);
+        }
     }
-    // exchange j of a frame (0..2T): even j carries L (to row owners), odd j E
-    const int per_frame = 2 * a.max_iter + 1;
+    // bytes arriving in an L exchange (ROW region) and an E exchange (VAR region)
+    uint32_t rx_l = 0, rx_e = 0;
+    for (int s = 0; s < C; ++s)
+        for (int h = 0; h < H; ++h)
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                rx_l += uint32_t(__ldg(sbytes + key(s, q, h, b)));
+                rx_e += uint32_t(__ldg(sbytes + key(q, s, h, b)));
+            }
     if (tt == 0) {
-        mbar_init(bar_s, 1);
-        mbar_init(bar_s + 8, 1);
-        mbar_init(free_s, C);
+        mbar_init(vbar, 1);
+        mbar_init(rbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        mbar_arm(bar_s, rx_l);                             // exchange 0: L
-        mbar_arm(bar_s + 8, per_frame > 1 ? rx_e : rx_l);  // exchange 1
+        mbar_arm(vbar, rx_e);
+        mbar_arm(rbar, rx_l);
     }
     cluster_sync_all();
 
-    uint32_t h = 0;      // exchanges completed by this CTA (over all frames)
-    // Exchange h: SEND -> RECV[h & 1] of every CTA of the cluster.  type_l:
-    // an L exchange (segment (q, d) from the send layout) or an E exchange
-    // (segment (d, q) from the receive layout).
-    auto exchange = [&](bool type_l, int j) {
+    uint32_t nl = 0, ne = 0;    // L / E exchanges completed (barrier phases)
+    // Ship V-phase chunk h: segments (q, d, h, b) of the VAR region -> ROW region of d.
+    auto ship_l = [&](int h) {
         fence_proxy_async_smem();
         __syncthreads();
-        const uint32_t x = h & 1u;
-        if (tt < C) {
-            const int d = tt;
-            const uint32_t src = type_l ? uint32_t(__ldg(sOff + q * C + d)) : uint32_t(__ldg(rOff + d * C + q));
-            const uint32_t dst = type_l ? uint32_t(__ldg(rOff + q * C + d)) : uint32_t(__ldg(sOff + d * C + q));
-            const uint32_t nbytes = uint32_t(__ldg(sbytes + (type_l ? q * C + d : d * C + q)));
+        if (tt < NB * C) {
+            const int b = tt / C, d = tt - b * C;
+            const int k = key(int(q), d, h, b);
+            const uint32_t nbytes = uint32_t(__ldg(sbytes + k));
             if (nbytes)
-                bulk_s2c(mapa_u32(recv_s + x * cap_b + dst, uint32_t(d)), send_s + src, nbytes,
-                         mapa_u32(bar_s + 8u * x, uint32_t(d)));
+                bulk_s2c(mapa_u32(row_s + uint32_t(__ldg(rowOff + k)), uint32_t(d)), var_s + uint32_t(__ldg(varOff + k)),
+                         nbytes, mapa_u32(rbar, uint32_t(d)));
         }
-        mbar_wait(bar_s + 8u * x, (h >> 1) & 1u);
-        if (tt == 0) {
-            int jn = j + 2;
-            if (jn >= per_frame) jn -= per_frame;
-            mbar_arm(bar_s + 8u * x, (jn & 1) ? rx_e : rx_l);
-        }
-        if (tt < C) mbar_arrive_remote(mapa_u32(free_s, uint32_t(tt)));
-        ++h;
     };
-    // SEND may be rewritten once every destination holds exchange h - 1.
-    auto send_free = [&]() {
-        if (h > 0) mbar_wait(free_s, (h - 1) & 1u);
+    // Ship C-phase band b: segments (s, q, h, b) of the ROW region -> VAR region of s.
+    auto ship_e = [&](int b) {
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tt < C * H) {
+            const int s = tt / H, h = tt - s * H;
+            const int k = key(s, int(q), h, b);
+            const uint32_t nbytes = uint32_t(__ldg(sbytes + k));
+            if (nbytes)
+                bulk_s2c(mapa_u32(var_s + uint32_t(__ldg(varOff + k)), uint32_t(s)), row_s + uint32_t(__ldg(rowOff + k)),
+                         nbytes, mapa_u32(vbar, uint32_t(s)));
+        }
+    };
+    auto wait_row = [&]() {
+        mbar_wait(rbar, nl & 1u);
+        if (tt == 0) mbar_arm(rbar, rx_l);
+        ++nl;
+    };
+    auto wait_var = [&]() {
+        mbar_wait(vbar, ne & 1u);
+        if (tt == 0) mbar_arm(vbar, rx_e);
+        ++ne;
     };
 
-    const uint16_t *ridx = code.xband_ridx, *sidx = code.xband_sidx;
     for (int64_t f = cid; f < a.frames; f += ncl) {
         const float *llr = a.llr + f * int64_t(n);
-        float e0[B0][WR];
-        uint32_t synd = 0;
-        // ---- V-phase 0 (a1/a2): L = R, E = 0; send L_vc = R; band-0 check of t = 1
-        send_free();
+        float e0[H][WR];
+        // ---- V-phase 0 (a1/a2): L = R, E = 0; L_vc = R; band-0 check of t = 1
 #pragma unroll
-        for (int k = 0; k < B0; ++k) {
-            const int r = tt + k * T;
+        for (int h = 0; h < H; ++h) {
+            const int r = tt + h * T;
             if (r < mbq) {
                 const int v0 = (int(q) * mbq + r) * WR;
                 float lv[WR];
-                lds_row<WR>(reinterpret_cast<const char *>(llr), uint32_t(v0) * 4u, lv);   // global, 8B aligned rows
+                lds_row<WR>(reinterpret_cast<const char *>(llr), uint32_t(v0) * 4u, lv);   // global, 8B-aligned rows
 #pragma unroll
                 for (int j = 0; j < WR; ++j) lv[j] = fminf(fmaxf(lv[j], -30.0f), 30.0f) * kL2E;
-                uint32_t sl[WR * NB];
-                ld_u16_row<WR * NB>(sidx + size_t(v0) * NB, sl);
+                const uint16_t *vt = vtab + size_t(r) * WR * NB;
 #pragma unroll
                 for (int j = 0; j < WR; ++j)
 #pragma unroll
-                    for (int b = 0; b < NB; ++b) *reinterpret_cast<float *>(send + sl[j * NB + b]) = lv[j];
-                check_row<WR, true>(lv, e0[k]);
+                    for (int b = 0; b < NB; ++b) *reinterpret_cast<float *>(varr + vt[j * NB + b]) = lv[j];
+                check_row<WR, true>(lv, e0[h]);
             }
+            ship_l(h);
         }
-        exchange(true, 0);
+        uint32_t synd = 0;
         for (int t = 1; t <= a.max_iter; ++t) {
-            const char *rin = recv0 + ((h - 1) & 1u) * cap_b;
-            // ---- C-phase t (a3): rows of bands >= 1 owned by q
-            send_free();
+            // ---- C-phase t (a3): rows of bands >= 1 owned by q, band by band
+            wait_row();
 #pragma unroll
-            for (int k = 0; k < B1; ++k) {
-                const int r = tt + k * T;
-                if (r < NB * mbq) {
-                    const int b = r / mbq, lr = r - b * mbq;
-                    uint32_t sl[WR];
-                    ld_u16_row<WR>(ridx + size_t(b) * n + size_t(int(q) * mbq + lr) * WR, sl);
-                    float x[WR], e[WR];
+            for (int b = 0; b < NB; ++b) {
 #pragma unroll
-                    for (int j = 0; j < WR; ++j) x[j] = *reinterpret_cast<const float *>(rin + sl[j]);
-                    check_row<WR, true>(x, e);
+                for (int k = 0; k < H; ++k) {
+                    const int lr = tt + k * T;
+                    if (lr < mbq) {
+                        const uint16_t *rt = rtab + (size_t(b) * mbq + lr) * WR;
+                        uint32_t sl[WR];
 #pragma unroll
-                    for (int j = 0; j < WR; ++j) *reinterpret_cast<float *>(send + sl[j]) = e[j];
+                        for (int j = 0; j < WR; ++j) sl[j] = rt[j];
+                        float x[WR], e[WR];
+#pragma unroll
+                        for (int j = 0; j < WR; ++j) x[j] = *reinterpret_cast<const float *>(rowr + sl[j]);
+                        check_row<WR, true>(x, e);
+#pragma unroll
+                        for (int j = 0; j < WR; ++j) *reinterpret_cast<float *>(rowr + sl[j]) = e[j];
+                    }
                 }
+                ship_e(b);
             }
-            exchange(false, 2 * t - 1);
-            // ---- V-phase t (a4/a5): L = R + sum E; send L_vc (L itself at t = T)
+            // ---- V-phase t (a4/a5): L = R + sum E; L_vc over the E slots (L itself at t = T)
             const bool last = t == a.max_iter;
-            rin = recv0 + ((h - 1) & 1u) * cap_b;
-            send_free();
+            wait_var();
 #pragma unroll
-            for (int k = 0; k < B0; ++k) {
-                const int r = tt + k * T;
+            for (int h = 0; h < H; ++h) {
+                const int r = tt + h * T;
                 if (r < mbq) {
                     const int v0 = (int(q) * mbq + r) * WR;
                     float lv[WR];
                     lds_row<WR>(reinterpret_cast<const char *>(llr), uint32_t(v0) * 4u, lv);
+                    const uint16_t *vt = vtab + size_t(r) * WR * NB;
                     uint32_t sl[WR * NB];
-                    ld_u16_row<WR * NB>(sidx + size_t(v0) * NB, sl);
+#pragma unroll
+                    for (int i = 0; i < WR * NB; ++i) sl[i] = vt[i];
                     float eb[WR * NB];
 #pragma unroll
                     for (int j = 0; j < WR; ++j) {
-                        lv[j] = fminf(fmaxf(lv[j], -30.0f), 30.0f) * kL2E + e0[k][j];
+                        lv[j] = fminf(fmaxf(lv[j], -30.0f), 30.0f) * kL2E + e0[h][j];
 #pragma unroll
                         for (int b = 0; b < NB; ++b) {
-                            eb[j * NB + b] = *reinterpret_cast<const float *>(rin + sl[j * NB + b]);
+                            eb[j * NB + b] = *reinterpret_cast<const float *>(varr + sl[j * NB + b]);
                             lv[j] += eb[j * NB + b];
                         }
                     }
@@ -282,7 +301,7 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
                         for (int j = 0; j < WR; ++j) {
                             rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
 #pragma unroll
-                            for (int b = 0; b < NB; ++b) *reinterpret_cast<float *>(send + sl[j * NB + b]) = lv[j];
+                            for (int b = 0; b < NB; ++b) *reinterpret_cast<float *>(varr + sl[j * NB + b]) = lv[j];
                         }
                         synd |= rp;
                     } else {
@@ -291,45 +310,39 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
                         for (int j = 0; j < WR; ++j) {
 #pragma unroll
                             for (int b = 0; b < NB; ++b)
-                                *reinterpret_cast<float *>(send + sl[j * NB + b]) = lv[j] - eb[j * NB + b];
-                            x[j] = lv[j] - e0[k][j];
+                                *reinterpret_cast<float *>(varr + sl[j * NB + b]) = lv[j] - eb[j * NB + b];
+                            x[j] = lv[j] - e0[h][j];
                         }
-                        check_row<WR, true>(x, e0[k]);
+                        check_row<WR, true>(x, e0[h]);
                     }
                 }
+                ship_l(h);
             }
-            exchange(true, 2 * t);
         }
-        // ---- a7: syndrome of z = [L >= 0]; rows of bands >= 1 see L at their slots
-        const char *lin = recv0 + ((h - 1) & 1u) * cap_b;
+        // ---- a7: syndrome of z = [L >= 0]: ROW slots now hold L (bands >= 1)
+        wait_row();
         for (int r = tt; r < NB * mbq; r += T) {
-            const int b = r / mbq, lr = r - b * mbq;
-            uint32_t sl[WR];
-            ld_u16_row<WR>(ridx + size_t(b) * n + size_t(int(q) * mbq + lr) * WR, sl);
+            const uint16_t *rt = rtab + size_t(r) * WR;
             uint32_t rp = 0;
 #pragma unroll
-            for (int j = 0; j < WR; ++j) rp ^= (*reinterpret_cast<const float *>(lin + sl[j]) >= 0.0f) ? 1u : 0u;
+            for (int j = 0; j < WR; ++j) rp ^= (*reinterpret_cast<const float *>(rowr + rt[j]) >= 0.0f) ? 1u : 0u;
             synd |= rp;
         }
         const int any = __syncthreads_or(synd != 0);
-        // final L in variable order, into the idle receive buffer (its last
-        // readers passed the barrier of exchange h - 1)
-        float *lfin = reinterpret_cast<float *>(recv0 + (h & 1u) * cap_b);
-        for (int i = tt; i < nq; i += T) {
-            const uint32_t s0 = __ldg(sidx + (size_t(q) * nq + i) * NB);
-            lfin[i] = *reinterpret_cast<const float *>(send + s0);
-        }
         if (tt == 0) {
             int *f0 = cg::this_cluster().map_shared_rank(flags, 0);
             f0[q] = any;
         }
         cluster_sync_all();
-        // ---- a6/a8: bits (words starting in q's variable range), posteriors, flags
+        // ---- a6/a8: bits (words starting in q's variable range), posteriors, flags.
+        // L_v sits in the VAR slot of (v, band 1) of its owner.
         {
             const int nw = code.nw;
             const int w_lo = (int(q) * nq + 31) / 32;
             const int w_hi = (int(q) == C - 1) ? nw : ((int(q) + 1) * nq + 31) / 32;
-            const float *lnext = (int(q) + 1 < C) ? cg::this_cluster().map_shared_rank(lfin, int(q) + 1) : lfin;
+            const int qn = (int(q) + 1 < C) ? int(q) + 1 : int(q);
+            const char *vnext = cg::this_cluster().map_shared_rank(varr, qn);
+            const uint16_t *tnext = cg::this_cluster().map_shared_rank(vtab, qn);
             uint32_t *bits = a.bits + f * int64_t(nw);
             // T is a multiple of 32: each warp covers whole words
             for (int base = w_lo * 32; base < w_hi * 32; base += T) {
@@ -338,14 +351,16 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
                 bool z = false;
                 if (v < n) {
                     const int i = v - int(q) * nq;
-                    z = (i < nq ? lfin[i] : lnext[i - nq]) >= 0.0f;
+                    const float lv = i < nq ? *reinterpret_cast<const float *>(varr + vtab[size_t(i) * NB])
+                                            : *reinterpret_cast<const float *>(vnext + tnext[size_t(i - nq) * NB]);
+                    z = lv >= 0.0f;
                 }
                 const uint32_t word = __ballot_sync(0xffffffffu, z);
                 if ((tt & 31) == 0) bits[v >> 5] = word;
             }
             if (a.posterior) {
                 float *dst = a.posterior + f * int64_t(n) + int64_t(q) * nq;
-                for (int i = tt; i < nq; i += T) dst[i] = lfin[i] * kLn2;
+                for (int i = tt; i < nq; i += T) dst[i] = *reinterpret_cast<const float *>(varr + vtab[size_t(i) * NB]) * kLn2;
             }
             if (q == 0 && tt == 0) {
                 int ok = 1;
@@ -354,23 +369,23 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
                 a.iters[f] = a.max_iter;
             }
         }
-        cluster_sync_all();     // lfin / flags are reused by the next frame
+        cluster_sync_all();     // VAR regions / flags are reused by the next frame
     }
 }
 
-template <int WR, int B0>
+template <int WR, int H>
 void *pick_x_c(int C) {
     switch (C) {
-        case 4: return reinterpret_cast<void *>(&xband_kernel<WR, 3, B0, 4>);
-        case 8: return reinterpret_cast<void *>(&xband_kernel<WR, 3, B0, 8>);
-        case 16: return reinterpret_cast<void *>(&xband_kernel<WR, 3, B0, 16>);
+        case 4: return reinterpret_cast<void *>(&xband_kernel<WR, 3, H, 4>);
+        case 8: return reinterpret_cast<void *>(&xband_kernel<WR, 3, H, 8>);
+        case 16: return reinterpret_cast<void *>(&xband_kernel<WR, 3, H, 16>);
     }
     return nullptr;
 }
 
-void *pick_xband_kernel(int wr, int wc, int b0, int C) {
+void *pick_xband_kernel(int wr, int wc, int H, int C) {
     if (wc != 3 || wr != 6) return nullptr;
-    switch (b0) {
+    switch (H) {
         case 1: return pick_x_c<6, 1>(C);
         case 2: return pick_x_c<6, 2>(C);
         case 4: return pick_x_c<6, 4>(C);
@@ -384,15 +399,14 @@ bool xcluster_plan(const ldpc_code &c, int64_t frames, bool et, XClusterPlan &p)
     if (et || !c.gallager || !c.regular_col || !c.dev.xcluster) return false;
     const int C = c.dev.xcluster;
     const int mbq = c.n / c.wr / C;
-    int b0 = std::max(1, (mbq + 1023) / 1024);
-    if (b0 == 3) b0 = 4;
-    void *k = pick_xband_kernel(c.wr, c.wc, b0, C);
+    const int H = xband_rows_per_thread(mbq);
+    void *k = pick_xband_kernel(c.wr, c.wc, H, C);
     if (!k) return false;
     p.kernel = k;
     p.cluster = C;
-    p.threads = ((mbq + b0 - 1) / b0 + 31) / 32 * 32;
-    if (p.threads * b0 * (c.wc - 1) < mbq * (c.wc - 1)) return false;
-    p.smem = 3 * size_t(c.dev.xcap) * 4 + 32 + 4 * size_t(C);
+    p.threads = xband_threads(mbq);
+    if (p.threads * H < mbq || p.threads < (c.wc - 1) * C || p.threads < C * H) return false;
+    p.smem = xband_smem_bytes(c.n, c.wc, c.wr, C);
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p.smem)) != cudaSuccess) return false;
     if (C > 8 && cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) return false;
     cudaLaunchConfig_t cfg = {};

@@ -7,7 +7,10 @@
 //           complete_tx on the receiver's mbarrier; free-barrier handshake
 //           (the decoder's protocol, no compute in between);
 //   st.v4 : all threads store 16-byte vectors to the remote CTAs
-//           (st.shared::cluster.v4), then a cluster barrier.
+//           (st.shared::cluster.v4), then a cluster barrier;
+//   l2.v4 : all threads store the send buffer to a global slot (L2-resident,
+//           16-byte vectors), cluster barrier, then load their segments from
+//           every CTA's slot (ld.global.cg.v4) into shared memory.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o microbench_bulk microbench_bulk.cu
 #include <cuda_runtime.h>
 
@@ -42,7 +45,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 }
 
 template <int C, int MODE>
-__global__ void kern(int bytes, int reps, unsigned long long *cycles) {
+__global__ void kern(int bytes, int reps, unsigned long long *cycles, float4 *gbuf) {
     extern __shared__ __align__(128) char smem[];
     const int tt = threadIdx.x, T = blockDim.x;
     const uint32_t q = ctarank();
@@ -80,6 +83,18 @@ __global__ void kern(int bytes, int reps, unsigned long long *cycles) {
             if (tt < C)
                 asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(mapa_u32(free_s, tt))
                              : "memory");
+        } else if (MODE == 2) {
+            float4 *mine = gbuf + size_t(blockIdx.x) * (bytes / 16);
+            for (int i = tt; i < bytes / 16; i += T) mine[i] = reinterpret_cast<const float4 *>(send)[i];
+            cluster_sync_all();
+            const int vec_per_seg = seg / 16;
+            const size_t cl0 = size_t(blockIdx.x - q);
+            for (int i = tt; i < bytes / 16; i += T) {
+                const int s = i / vec_per_seg, o = i - s * vec_per_seg;
+                const float4 v = __ldcg(gbuf + (cl0 + s) * (bytes / 16) + q * vec_per_seg + o);
+                reinterpret_cast<float4 *>(recv + x * bytes)[i] = v;
+            }
+            __syncthreads();
         } else {
             // every thread stores 16-byte vectors: destination d = i / (seg/16)
             const int vec_per_seg = seg / 16;
@@ -122,7 +137,9 @@ void run(int sms, unsigned long long *d_cyc, int bytes, int threads) {
     cudaOccupancyMaxActiveClusters(&ncl, k, &cfg);
     grid = std::min(grid, ncl * C);
     cfg.gridDim = dim3(grid);
-    for (int rep = 0; rep < 2; ++rep) cudaLaunchKernelEx(&cfg, k, bytes, reps, d_cyc);
+    float4 *gbuf = nullptr;
+    cudaMalloc(&gbuf, size_t(grid) * bytes);
+    for (int rep = 0; rep < 2; ++rep) cudaLaunchKernelEx(&cfg, k, bytes, reps, d_cyc, gbuf);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         printf("error %s\n", cudaGetErrorString(e));
@@ -130,12 +147,13 @@ void run(int sms, unsigned long long *d_cyc, int bytes, int threads) {
     }
     std::vector<unsigned long long> cyc(grid);
     cudaMemcpy(cyc.data(), d_cyc, sizeof(unsigned long long) * grid, cudaMemcpyDeviceToHost);
+    cudaFree(gbuf);
     double mean = 0;
     for (auto c : cyc) mean += double(c);
     mean /= grid;
     const double per = mean / reps;
     printf("%-5s C=%2d clusters=%3d threads=%4d bytes/CTA=%6d : %8.0f clk/exchange  %6.1f B/clk/SM out\n",
-           MODE == 0 ? "bulk" : "st.v4", C, grid / C, threads, bytes, per, bytes / per);
+           MODE == 0 ? "bulk" : (MODE == 1 ? "st.v4" : "l2.v4"), C, grid / C, threads, bytes, per, bytes / per);
 }
 
 int main() {
@@ -146,6 +164,10 @@ int main() {
     for (int bytes : {2048, 16384, 49152}) {
         run<8, 0>(sms, d_cyc, bytes, 1024);
         run<8, 1>(sms, d_cyc, bytes, 1024);
+        run<8, 2>(sms, d_cyc, bytes, 1024);
+        run<4, 2>(sms, d_cyc, bytes, 1024);
+        run<2, 2>(sms, d_cyc, bytes, 1024);
+        run<1, 2>(sms, d_cyc, bytes, 1024);
         run<4, 0>(sms, d_cyc, bytes, 1024);
         run<4, 1>(sms, d_cyc, bytes, 1024);
         run<16, 0>(sms, d_cyc, bytes / 2, 1024);
