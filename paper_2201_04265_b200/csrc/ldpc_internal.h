@@ -86,7 +86,8 @@ inline int band_cluster_size(int32_t n, int32_t wc, int32_t wr) {
 
 // Exchange cluster kernel (spa_cluster.cu): C CTAs per frame, CTA q owns
 // mbq = n / wr / C rows of every band and the nq = mbq wr variables of its
-// band-0 rows.  Threads and rows per thread (= V-phase chunks H) of a CTA:
+// band-0 rows.  Compute threads and rows per thread (= V-phase chunks H) of a
+// CTA (the launch adds one producer warp):
 inline int xband_rows_per_thread(int32_t mbq) {
     const int b0 = mbq > 0 ? (mbq + 1023) / 1024 : 1;
     return b0 == 3 ? 4 : b0;                      // instantiated: 1, 2, 4
@@ -106,7 +107,7 @@ inline int32_t xband_capacity(int32_t n, int32_t wc, int32_t wr, int32_t C) {
 // + barriers and flags.
 inline size_t xband_smem_bytes(int32_t n, int32_t wc, int32_t wr, int32_t C) {
     const size_t nq = size_t(n / wr / C) * size_t(wr);
-    return 2 * size_t(xband_capacity(n, wc, wr, C)) * 4 + 2 * size_t(wc - 1) * nq * 2 + 32 + 4 * size_t(C);
+    return 2 * size_t(xband_capacity(n, wc, wr, C)) * 4 + 2 * size_t(wc - 1) * nq * 2 + 16 + 8 * 16 + 4 * size_t(C);
 }
 // The smallest power of two C <= 16 with mb % C == 0 whose shared memory fits
 // one CTA and whose region offsets fit 16 bits; 0 when a frame fits one SM or
@@ -117,7 +118,7 @@ inline int xband_cluster_size(int32_t n, int32_t wc, int32_t wr) {
     for (int C = 2; C <= 16; C *= 2) {
         if ((n / wr) % C) continue;
         if (size_t(xband_capacity(n, wc, wr, C)) * 4 > 65532) continue;
-        if (xband_threads(n / wr / C) > 1024) continue;
+        if (xband_threads(n / wr / C) + 32 > 1024) continue;      // + the producer warp
         if (xband_smem_bytes(n, wc, wr, C) + 1024 <= 227 * 1024) return C;
     }
     return 0;

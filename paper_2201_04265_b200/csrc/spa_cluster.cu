@@ -20,7 +20,9 @@
 //            row chunk h, ship its segments (one per (band, row owner)) to the
 //            owners' ROW regions.
 // Shipping = cp.async.bulk shared::cta -> shared::cluster, complete_tx on the
-// receiver's region barrier; early chunks travel while later chunks compute.
+// receiver's region barrier, issued by a producer warp as soon as the compute
+// warps have arrived on the chunk's barrier: early chunks travel while later
+// chunks compute, and no CTA-wide barrier sits inside the iteration loop.
 // Random remote 4-byte DSMEM accesses run at ~0.4/clk/SM and bulk segment
 // exchange at ~12 B/clk/SM (profiles/r01_microbench*.txt), hence the segments
 // and the overlap.  The two slot tables of the CTA are copied to shared memory
@@ -135,15 +137,25 @@ struct XArgs {
     float *posterior;
 };
 
+__device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
 // Shared memory: VAR region | ROW region (cap floats each) | var slot table
-// u16 [nq][NB] | row slot table u16 [NB][mbq][WR] | var_bar, row_bar | flags[C]
+// u16 [nq][NB] | row slot table u16 [NB][mbq][WR] | barriers | flags[C].
+// Barriers: var_bar, row_bar (incoming E / L exchange, complete_tx),
+// vchunk[H], cchunk[NB] (compute warps finished a chunk).
+// Warps: TW / 32 compute warps, then one producer warp that ships each chunk
+// as soon as every compute warp arrived on its chunk barrier -- no CTA-wide
+// barrier inside the iteration loop.
 template <int WR, int WC, int H, int C>
 __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
     extern __shared__ __align__(128) char smem[];
     constexpr int NB = WC - 1;
     const DeviceCode &code = a.code;
     const int n = code.n, mb = code.mb, mbq = mb / C, nq = n / C;
-    const int T = blockDim.x, tt = threadIdx.x;
+    const int TW = blockDim.x - 32, tt = threadIdx.x, lane = tt & 31;
+    const bool producer = tt >= TW;
     const uint32_t cap_b = uint32_t(code.xcap) * 4u;
     const uint32_t q = cluster_ctarank();
     const int64_t cid = cluster_id_x(), ncl = ncluster_x();
@@ -152,8 +164,9 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
     uint16_t *vtab = reinterpret_cast<uint16_t *>(smem + 2 * cap_b);
     uint16_t *rtab = vtab + size_t(nq) * NB;
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + ((2 * cap_b + 4u * uint32_t(NB * nq) + 15u) & ~15u));
-    int *flags = reinterpret_cast<int *>(bars + 2);
+    int *flags = reinterpret_cast<int *>(bars + 2 + H + NB);
     const uint32_t var_s = saddr(varr), row_s = saddr(rowr), vbar = saddr(bars), rbar = vbar + 8;
+    const uint32_t vchunk = vbar + 16, cchunk = vchunk + 8 * H;
     const int nkey = C * C * H * NB;
     const int32_t *varOff = code.xband_seg, *rowOff = code.xband_seg + nkey, *sbytes = code.xband_seg + 2 * nkey;
     auto key = [](int s, int d, int h, int b) { return ((s * C + d) * H + h) * NB + b; };
@@ -162,11 +175,11 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
     {
         const uint32_t *src = reinterpret_cast<const uint32_t *>(code.xband_sidx + size_t(q) * nq * NB);
         uint32_t *dst = reinterpret_cast<uint32_t *>(vtab);
-        for (int i = tt; i < nq * NB / 2; i += T) dst[i] = __ldg(src + i);
+        for (int i = tt; i < nq * NB / 2; i += blockDim.x) dst[i] = __ldg(src + i);
         for (int b = 0; b < NB; ++b) {
             const uint32_t *rs = reinterpret_cast<const uint32_t *>(code.xband_ridx + size_t(b) * n + size_t(q) * mbq * WR);
             uint32_t *rd = reinterpret_cast<uint32_t *>(rtab + size_t(b) * mbq * WR);
-            for (int i = tt; i < mbq * WR / 2; i += T) rd[i] = __ldg(rs + i);
+            for (int i = tt; i < mbq * WR / 2; i += blockDim.x) rd[i] = __ldg(rs + i);
         }
     }
     // bytes arriving in an L exchange (ROW region) and an E exchange (VAR region)
@@ -181,19 +194,26 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
     if (tt == 0) {
         mbar_init(vbar, 1);
         mbar_init(rbar, 1);
+        for (int i = 0; i < H + NB; ++i) mbar_init(vchunk + 8 * i, uint32_t(TW / 32));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         mbar_arm(vbar, rx_e);
         mbar_arm(rbar, rx_l);
     }
     cluster_sync_all();
 
-    uint32_t nl = 0, ne = 0;    // L / E exchanges completed (barrier phases)
-    // Ship V-phase chunk h: segments (q, d, h, b) of the VAR region -> ROW region of d.
-    auto ship_l = [&](int h) {
+    // compute warps: one arrival per warp on a chunk barrier, after making the
+    // lanes' shared-memory writes visible to the async (bulk-copy) proxy
+    auto chunk_done = [&](uint32_t bar) {
         fence_proxy_async_smem();
-        __syncthreads();
-        if (tt < NB * C) {
-            const int b = tt / C, d = tt - b * C;
+        __syncwarp();
+        if (lane == 0) mbar_arrive_local(bar);
+    };
+    uint32_t nv = 0, nc = 0;    // V / C phases shipped (producer: chunk barrier phases)
+    // producer: ship V chunk h (segments (q, d, h, b): VAR region -> ROW region of d)
+    auto ship_l = [&](int h) {
+        mbar_wait(vchunk + 8 * h, nv & 1u);
+        if (lane < NB * C) {
+            const int b = lane / C, d = lane - b * C;
             const int k = key(int(q), d, h, b);
             const uint32_t nbytes = uint32_t(__ldg(sbytes + k));
             if (nbytes)
@@ -201,12 +221,11 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
                          nbytes, mapa_u32(rbar, uint32_t(d)));
         }
     };
-    // Ship C-phase band b: segments (s, q, h, b) of the ROW region -> VAR region of s.
+    // producer: ship C chunk b (segments (s, q, h, b): ROW region -> VAR region of s)
     auto ship_e = [&](int b) {
-        fence_proxy_async_smem();
-        __syncthreads();
-        if (tt < C * H) {
-            const int s = tt / H, h = tt - s * H;
+        mbar_wait(cchunk + 8 * b, nc & 1u);
+        if (lane < C * H) {
+            const int s = lane / H, h = lane - s * H;
             const int k = key(s, int(q), h, b);
             const uint32_t nbytes = uint32_t(__ldg(sbytes + k));
             if (nbytes)
@@ -214,6 +233,7 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
                          nbytes, mapa_u32(vbar, uint32_t(s)));
         }
     };
+    uint32_t nl = 0, ne = 0;    // compute warps: L / E exchanges received
     auto wait_row = [&]() {
         mbar_wait(rbar, nl & 1u);
         if (tt == 0) mbar_arm(rbar, rx_l);
@@ -228,105 +248,120 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
     for (int64_t f = cid; f < a.frames; f += ncl) {
         const float *llr = a.llr + f * int64_t(n);
         float e0[H][WR];
-        // ---- V-phase 0 (a1/a2): L = R, E = 0; L_vc = R; band-0 check of t = 1
-#pragma unroll
-        for (int h = 0; h < H; ++h) {
-            const int r = tt + h * T;
-            if (r < mbq) {
-                const int v0 = (int(q) * mbq + r) * WR;
-                float lv[WR];
-                lds_row<WR>(reinterpret_cast<const char *>(llr), uint32_t(v0) * 4u, lv);   // global, 8B-aligned rows
-#pragma unroll
-                for (int j = 0; j < WR; ++j) lv[j] = fminf(fmaxf(lv[j], -30.0f), 30.0f) * kL2E;
-                const uint16_t *vt = vtab + size_t(r) * WR * NB;
-#pragma unroll
-                for (int j = 0; j < WR; ++j)
-#pragma unroll
-                    for (int b = 0; b < NB; ++b) *reinterpret_cast<float *>(varr + vt[j * NB + b]) = lv[j];
-                check_row<WR, true>(lv, e0[h]);
-            }
-            ship_l(h);
-        }
         uint32_t synd = 0;
-        for (int t = 1; t <= a.max_iter; ++t) {
-            // ---- C-phase t (a3): rows of bands >= 1 owned by q, band by band
-            wait_row();
+        if (producer) {
+            // the producer's view of the frame: V0, then (C, V) x max_iter
 #pragma unroll
-            for (int b = 0; b < NB; ++b) {
+            for (int h = 0; h < H; ++h) ship_l(h);
+            ++nv;
+            for (int t = 1; t <= a.max_iter; ++t) {
 #pragma unroll
-                for (int k = 0; k < H; ++k) {
-                    const int lr = tt + k * T;
-                    if (lr < mbq) {
-                        const uint16_t *rt = rtab + (size_t(b) * mbq + lr) * WR;
-                        uint32_t sl[WR];
+                for (int b = 0; b < NB; ++b) ship_e(b);
+                ++nc;
 #pragma unroll
-                        for (int j = 0; j < WR; ++j) sl[j] = rt[j];
-                        float x[WR], e[WR];
-#pragma unroll
-                        for (int j = 0; j < WR; ++j) x[j] = *reinterpret_cast<const float *>(rowr + sl[j]);
-                        check_row<WR, true>(x, e);
-#pragma unroll
-                        for (int j = 0; j < WR; ++j) *reinterpret_cast<float *>(rowr + sl[j]) = e[j];
-                    }
-                }
-                ship_e(b);
+                for (int h = 0; h < H; ++h) ship_l(h);
+                ++nv;
             }
-            // ---- V-phase t (a4/a5): L = R + sum E; L_vc over the E slots (L itself at t = T)
-            const bool last = t == a.max_iter;
-            wait_var();
+        } else {
+            // ---- V-phase 0 (a1/a2): L = R, E = 0; L_vc = R; band-0 check of t = 1
 #pragma unroll
             for (int h = 0; h < H; ++h) {
-                const int r = tt + h * T;
+                const int r = tt + h * TW;
                 if (r < mbq) {
                     const int v0 = (int(q) * mbq + r) * WR;
                     float lv[WR];
-                    lds_row<WR>(reinterpret_cast<const char *>(llr), uint32_t(v0) * 4u, lv);
+                    lds_row<WR>(reinterpret_cast<const char *>(llr), uint32_t(v0) * 4u, lv);   // global, 8B-aligned rows
+#pragma unroll
+                    for (int j = 0; j < WR; ++j) lv[j] = fminf(fmaxf(lv[j], -30.0f), 30.0f) * kL2E;
                     const uint16_t *vt = vtab + size_t(r) * WR * NB;
-                    uint32_t sl[WR * NB];
 #pragma unroll
-                    for (int i = 0; i < WR * NB; ++i) sl[i] = vt[i];
-                    float eb[WR * NB];
+                    for (int j = 0; j < WR; ++j)
 #pragma unroll
-                    for (int j = 0; j < WR; ++j) {
-                        lv[j] = fminf(fmaxf(lv[j], -30.0f), 30.0f) * kL2E + e0[h][j];
-#pragma unroll
-                        for (int b = 0; b < NB; ++b) {
-                            eb[j * NB + b] = *reinterpret_cast<const float *>(varr + sl[j * NB + b]);
-                            lv[j] += eb[j * NB + b];
-                        }
-                    }
-                    if (last) {
-                        uint32_t rp = 0;      // band-0 row syndrome bit (Eq. 1)
-#pragma unroll
-                        for (int j = 0; j < WR; ++j) {
-                            rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
-#pragma unroll
-                            for (int b = 0; b < NB; ++b) *reinterpret_cast<float *>(varr + sl[j * NB + b]) = lv[j];
-                        }
-                        synd |= rp;
-                    } else {
-                        float x[WR];
-#pragma unroll
-                        for (int j = 0; j < WR; ++j) {
-#pragma unroll
-                            for (int b = 0; b < NB; ++b)
-                                *reinterpret_cast<float *>(varr + sl[j * NB + b]) = lv[j] - eb[j * NB + b];
-                            x[j] = lv[j] - e0[h][j];
-                        }
-                        check_row<WR, true>(x, e0[h]);
-                    }
+                        for (int b = 0; b < NB; ++b) *reinterpret_cast<float *>(varr + vt[j * NB + b]) = lv[j];
+                    check_row<WR, true>(lv, e0[h]);
                 }
-                ship_l(h);
+                chunk_done(vchunk + 8 * h);
             }
-        }
-        // ---- a7: syndrome of z = [L >= 0]: ROW slots now hold L (bands >= 1)
-        wait_row();
-        for (int r = tt; r < NB * mbq; r += T) {
-            const uint16_t *rt = rtab + size_t(r) * WR;
-            uint32_t rp = 0;
+            for (int t = 1; t <= a.max_iter; ++t) {
+                // ---- C-phase t (a3): rows of bands >= 1 owned by q, band by band
+                wait_row();
 #pragma unroll
-            for (int j = 0; j < WR; ++j) rp ^= (*reinterpret_cast<const float *>(rowr + rt[j]) >= 0.0f) ? 1u : 0u;
-            synd |= rp;
+                for (int b = 0; b < NB; ++b) {
+#pragma unroll
+                    for (int k = 0; k < H; ++k) {
+                        const int lr = tt + k * TW;
+                        if (lr < mbq) {
+                            const uint16_t *rt = rtab + (size_t(b) * mbq + lr) * WR;
+                            uint32_t sl[WR];
+#pragma unroll
+                            for (int j = 0; j < WR; ++j) sl[j] = rt[j];
+                            float x[WR], e[WR];
+#pragma unroll
+                            for (int j = 0; j < WR; ++j) x[j] = *reinterpret_cast<const float *>(rowr + sl[j]);
+                            check_row<WR, true>(x, e);
+#pragma unroll
+                            for (int j = 0; j < WR; ++j) *reinterpret_cast<float *>(rowr + sl[j]) = e[j];
+                        }
+                    }
+                    chunk_done(cchunk + 8 * b);
+                }
+                // ---- V-phase t (a4/a5): L = R + sum E; L_vc over the E slots (L itself at t = T)
+                const bool last = t == a.max_iter;
+                wait_var();
+#pragma unroll
+                for (int h = 0; h < H; ++h) {
+                    const int r = tt + h * TW;
+                    if (r < mbq) {
+                        const int v0 = (int(q) * mbq + r) * WR;
+                        float lv[WR];
+                        lds_row<WR>(reinterpret_cast<const char *>(llr), uint32_t(v0) * 4u, lv);
+                        const uint16_t *vt = vtab + size_t(r) * WR * NB;
+                        uint32_t sl[WR * NB];
+#pragma unroll
+                        for (int i = 0; i < WR * NB; ++i) sl[i] = vt[i];
+                        float eb[WR * NB];
+#pragma unroll
+                        for (int j = 0; j < WR; ++j) {
+                            lv[j] = fminf(fmaxf(lv[j], -30.0f), 30.0f) * kL2E + e0[h][j];
+#pragma unroll
+                            for (int b = 0; b < NB; ++b) {
+                                eb[j * NB + b] = *reinterpret_cast<const float *>(varr + sl[j * NB + b]);
+                                lv[j] += eb[j * NB + b];
+                            }
+                        }
+                        if (last) {
+                            uint32_t rp = 0;      // band-0 row syndrome bit (Eq. 1)
+#pragma unroll
+                            for (int j = 0; j < WR; ++j) {
+                                rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
+#pragma unroll
+                                for (int b = 0; b < NB; ++b) *reinterpret_cast<float *>(varr + sl[j * NB + b]) = lv[j];
+                            }
+                            synd |= rp;
+                        } else {
+                            float x[WR];
+#pragma unroll
+                            for (int j = 0; j < WR; ++j) {
+#pragma unroll
+                                for (int b = 0; b < NB; ++b)
+                                    *reinterpret_cast<float *>(varr + sl[j * NB + b]) = lv[j] - eb[j * NB + b];
+                                x[j] = lv[j] - e0[h][j];
+                            }
+                            check_row<WR, true>(x, e0[h]);
+                        }
+                    }
+                    chunk_done(vchunk + 8 * h);
+                }
+            }
+            // ---- a7: syndrome of z = [L >= 0]: ROW slots now hold L (bands >= 1)
+            wait_row();
+            for (int r = tt; r < NB * mbq; r += TW) {
+                const uint16_t *rt = rtab + size_t(r) * WR;
+                uint32_t rp = 0;
+#pragma unroll
+                for (int j = 0; j < WR; ++j) rp ^= (*reinterpret_cast<const float *>(rowr + rt[j]) >= 0.0f) ? 1u : 0u;
+                synd |= rp;
+            }
         }
         const int any = __syncthreads_or(synd != 0);
         if (tt == 0) {
@@ -336,7 +371,7 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
         cluster_sync_all();
         // ---- a6/a8: bits (words starting in q's variable range), posteriors, flags.
         // L_v sits in the VAR slot of (v, band 1) of its owner.
-        {
+        if (!producer) {
             const int nw = code.nw;
             const int w_lo = (int(q) * nq + 31) / 32;
             const int w_hi = (int(q) == C - 1) ? nw : ((int(q) + 1) * nq + 31) / 32;
@@ -344,8 +379,8 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
             const char *vnext = cg::this_cluster().map_shared_rank(varr, qn);
             const uint16_t *tnext = cg::this_cluster().map_shared_rank(vtab, qn);
             uint32_t *bits = a.bits + f * int64_t(nw);
-            // T is a multiple of 32: each warp covers whole words
-            for (int base = w_lo * 32; base < w_hi * 32; base += T) {
+            // TW is a multiple of 32: each warp covers whole words
+            for (int base = w_lo * 32; base < w_hi * 32; base += TW) {
                 const int v = base + tt;
                 if (v >= w_hi * 32) break;          // warp-uniform
                 bool z = false;
@@ -356,11 +391,11 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
                     z = lv >= 0.0f;
                 }
                 const uint32_t word = __ballot_sync(0xffffffffu, z);
-                if ((tt & 31) == 0) bits[v >> 5] = word;
+                if (lane == 0) bits[v >> 5] = word;
             }
             if (a.posterior) {
                 float *dst = a.posterior + f * int64_t(n) + int64_t(q) * nq;
-                for (int i = tt; i < nq; i += T) dst[i] = *reinterpret_cast<const float *>(varr + vtab[size_t(i) * NB]) * kLn2;
+                for (int i = tt; i < nq; i += TW) dst[i] = *reinterpret_cast<const float *>(varr + vtab[size_t(i) * NB]) * kLn2;
             }
             if (q == 0 && tt == 0) {
                 int ok = 1;
@@ -404,8 +439,8 @@ bool xcluster_plan(const ldpc_code &c, int64_t frames, bool et, XClusterPlan &p)
     if (!k) return false;
     p.kernel = k;
     p.cluster = C;
-    p.threads = xband_threads(mbq);
-    if (p.threads * H < mbq || p.threads < (c.wc - 1) * C || p.threads < C * H) return false;
+    p.threads = xband_threads(mbq) + 32;          // compute warps + the producer warp
+    if ((p.threads - 32) * H < mbq || (c.wc - 1) * C > 32 || C * H > 32) return false;
     p.smem = xband_smem_bytes(c.n, c.wc, c.wr, C);
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p.smem)) != cudaSuccess) return false;
     if (C > 8 && cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) return false;
