@@ -96,7 +96,7 @@ DeviceLayout compute_layout(const ldpc_code &c, bool with_G) {
             L.xband_ridx = off; off = align256(off + sizeof(uint16_t) * nb);
             L.xband_sidx = off; off = align256(off + sizeof(uint16_t) * nb);
             const size_t H = size_t(xband_rows_per_thread(c.n / c.wr / C));
-            L.xband_seg = off;  off = align256(off + sizeof(int32_t) * 3 * size_t(C) * size_t(C) * H * size_t(c.wc - 1));
+            L.xband_seg = off;  off = align256(off + sizeof(int32_t) * 3 * size_t(C) * size_t(C) * H * H * size_t(c.wc - 1));
         }
     }
     if (with_G) {
@@ -112,53 +112,60 @@ DeviceLayout compute_layout(const ldpc_code &c, bool with_G) {
 
 // Message-segment tables of the exchange cluster kernel (spa_cluster.cu).
 // CTA q owns band rows [q mbq, (q+1) mbq) of every band and the variables
-// [q nq, (q+1) nq) of its band-0 rows; its local band-0 row rl is processed in
-// V-phase chunk h = rl / T (T = xband_threads(mbq)).  Every band-b >= 1 edge
-// (b, p) joins variable owner s = pi_b[p] / nq (chunk h of its variable) and
-// row owner d = (p / wr) / mbq.  The edge has ONE slot in s's VAR region
-// (E_cv arrives there, L_vc is written over it) and ONE slot in d's ROW region
-// (L_vc arrives there, E_cv is written over it).  Edges sharing (s, d, h, b)
-// form a segment, contiguous and in ascending p in both regions:
-//   var region of s: segments ordered by (h, b, d)   -- V-phase chunk h ships
-//                                                      its NB C segments at once
-//   row region of d: segments ordered by (b, s, h)   -- C-phase band b ships
-//                                                      its C H segments at once
+// [q nq, (q+1) nq) of its band-0 rows.  With T = xband_threads(mbq) compute
+// threads and H = xband_rows_per_thread(mbq), local band-0 row rl is
+// processed in V-phase chunk h = rl / T, and local row lr of band b >= 1 in
+// C-phase chunk c = (b-1) H + lr / T.  Every band-b >= 1 edge (b, p) joins
+// variable owner s = pi_b[p] / nq and row owner d = (p / wr) / mbq.  The edge
+// has ONE slot in s's VAR region (E_cv arrives there, L_vc is written over
+// it) and ONE in d's ROW region (L_vc arrives there, E_cv is written over it).
+// Edges sharing (s, d, h, c) form a segment, contiguous and in ascending p in
+// both regions:
+//   var region of s: segments ordered by (h, d, c) -- V chunk h ships its
+//                                                    C NC segments (NC = (wc-1) H)
+//   row region of d: segments ordered by (c, s, h) -- C chunk c ships its C H
 // Segments are padded to 16 bytes (bulk-copy granularity).  Outputs:
 //   ridx[(b-1) n + p]    = byte slot of edge (b, p) in d's row region
 //   sidx[v (wc-1) + b-1] = byte slot of edge (b, pi_b^-1(v)) in s's var region
 //   seg = { varOff, rowOff, bytes }, three int32 arrays indexed by
-//         key(s, d, h, b) = ((s C + d) H + h) (wc-1) + (b-1).
-void xband_tables(const ldpc_code &c, int C, std::vector<uint16_t> &ridx, std::vector<uint16_t> &sidx,
-                  std::vector<int32_t> &seg) {
+//         key(s, d, h, c) = ((s C + d) H + h) NC + c.
+// Returns the exact region capacity in floats (the largest region).
+int32_t xband_tables(const ldpc_code &c, int C, std::vector<uint16_t> &ridx, std::vector<uint16_t> &sidx,
+                     std::vector<int32_t> &seg) {
     const int32_t n = c.n, wc = c.wc, wr = c.wr, NB = wc - 1, mbq = n / wr / C, nq = mbq * wr;
-    const int32_t T = xband_threads(mbq), H = xband_rows_per_thread(mbq);
-    const size_t nb = size_t(NB) * size_t(n), nkey = size_t(C) * C * H * NB;
-    auto key = [&](int32_t s, int32_t d, int32_t h, int32_t b) { return ((size_t(s) * C + d) * H + h) * NB + b; };
+    const int32_t T = xband_threads(mbq), H = xband_rows_per_thread(mbq), NC = NB * H;
+    const size_t nb = size_t(NB) * size_t(n), nkey = size_t(C) * C * H * NC;
+    auto key = [&](int32_t s, int32_t d, int32_t h, int32_t ch) { return ((size_t(s) * C + d) * H + h) * NC + ch; };
     std::vector<int32_t> cnt(nkey, 0), rank(nb), kof(nb);
     for (int32_t b = 0; b < NB; ++b)
         for (int32_t p = 0; p < n; ++p) {
             const int32_t v = c.col_idx[size_t(b + 1) * n + p];
             const int32_t s = v / nq, d = (p / wr) / mbq, h = ((v - s * nq) / wr) / T;
-            const size_t k = key(s, d, h, b);
+            const int32_t ch = b * H + ((p / wr) - d * mbq) / T;
+            const size_t k = key(s, d, h, ch);
             kof[size_t(b) * n + p] = int32_t(k);
             rank[size_t(b) * n + p] = cnt[k]++;
         }
     auto pad = [](int32_t x) { return (x + 3) & ~3; };
     seg.assign(3 * nkey, 0);
     int32_t *varOff = seg.data(), *rowOff = seg.data() + nkey, *bytes = seg.data() + 2 * nkey;
+    int32_t cap = 0;
     for (int32_t s = 0; s < C; ++s) {
         int32_t o = 0;
         for (int32_t h = 0; h < H; ++h)
-            for (int32_t b = 0; b < NB; ++b)
-                for (int32_t d = 0; d < C; ++d) { varOff[key(s, d, h, b)] = 4 * o; o += pad(cnt[key(s, d, h, b)]); }
+            for (int32_t d = 0; d < C; ++d)
+                for (int32_t ch = 0; ch < NC; ++ch) { varOff[key(s, d, h, ch)] = 4 * o; o += pad(cnt[key(s, d, h, ch)]); }
+        cap = std::max(cap, o);
     }
     for (int32_t d = 0; d < C; ++d) {
         int32_t o = 0;
-        for (int32_t b = 0; b < NB; ++b)
+        for (int32_t ch = 0; ch < NC; ++ch)
             for (int32_t s = 0; s < C; ++s)
-                for (int32_t h = 0; h < H; ++h) { rowOff[key(s, d, h, b)] = 4 * o; o += pad(cnt[key(s, d, h, b)]); }
+                for (int32_t h = 0; h < H; ++h) { rowOff[key(s, d, h, ch)] = 4 * o; o += pad(cnt[key(s, d, h, ch)]); }
+        cap = std::max(cap, o);
     }
     for (size_t i = 0; i < nkey; ++i) bytes[i] = 4 * pad(cnt[i]);
+    if (cap > kXbandMaxCapacity) return cap;     // 16-bit byte slots overflow: the caller drops the view
     ridx.assign(nb, 0);
     sidx.assign(nb, 0);
     for (int32_t b = 0; b < NB; ++b)
@@ -169,6 +176,7 @@ void xband_tables(const ldpc_code &c, int C, std::vector<uint16_t> &ridx, std::v
             ridx[size_t(b) * n + p] = uint16_t(rowOff[k] + 4 * r);
             sidx[size_t(v) * NB + b] = uint16_t(varOff[k] + 4 * r);
         }
+    return cap;
 }
 }  // namespace ldpc
 
@@ -422,6 +430,7 @@ ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, vo
               put(L.var_ptr, code->var_ptr.data(), sizeof(int32_t) * code->var_ptr.size()) &&
               put(L.var_edges, code->var_edges.data(), sizeof(int32_t) * code->var_edges.size());
     std::vector<int32_t> lidx, vpos;
+    int32_t xcap = 0;      // exact exchange-region capacity (0: no exchange view)
     if (ok && code->gallager && code->wc >= 2) {
         // Band view: edge (band b >= 1, position p) of row b*mb + p/wr is CSR edge
         // b*n + p (ldpc_make_H orders rows band-major, slots in pi_b order).
@@ -467,10 +476,11 @@ ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, vo
         if (ok && X > 0) {
             std::vector<uint16_t> ridx, sidx;
             std::vector<int32_t> seg;
-            ldpc::xband_tables(*code, X, ridx, sidx, seg);
-            ok = put(L.xband_ridx, ridx.data(), sizeof(uint16_t) * ridx.size()) &&
-                 put(L.xband_sidx, sidx.data(), sizeof(uint16_t) * sidx.size()) &&
-                 put(L.xband_seg, seg.data(), sizeof(int32_t) * seg.size());
+            xcap = ldpc::xband_tables(*code, X, ridx, sidx, seg);
+            if (xcap <= ldpc::kXbandMaxCapacity)
+                ok = put(L.xband_ridx, ridx.data(), sizeof(uint16_t) * ridx.size()) &&
+                     put(L.xband_sidx, sidx.data(), sizeof(uint16_t) * sidx.size()) &&
+                     put(L.xband_seg, seg.data(), sizeof(int32_t) * seg.size());
         }
     }
     if (ok && code->has_G)
@@ -505,8 +515,9 @@ ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, vo
     D.cluster = (code->gallager && code->wc >= 2) ? ldpc::band_cluster_size(code->n, code->wc, code->wr) : 0;
     D.cband_lidx = D.cluster ? reinterpret_cast<const int32_t *>(base + L.cband_lidx) : nullptr;
     D.cband_vpos = D.cluster ? reinterpret_cast<const int32_t *>(base + L.cband_vpos) : nullptr;
-    D.xcluster = (code->gallager && code->wc >= 2) ? ldpc::xband_cluster_size(code->n, code->wc, code->wr) : 0;
-    D.xcap = D.xcluster ? ldpc::xband_capacity(code->n, code->wc, code->wr, D.xcluster) : 0;
+    D.xcluster = (code->gallager && code->wc >= 2 && xcap > 0 && xcap <= ldpc::kXbandMaxCapacity)
+                     ? ldpc::xband_cluster_size(code->n, code->wc, code->wr) : 0;
+    D.xcap = D.xcluster ? xcap : 0;
     D.xband_ridx = D.xcluster ? reinterpret_cast<const uint16_t *>(base + L.xband_ridx) : nullptr;
     D.xband_sidx = D.xcluster ? reinterpret_cast<const uint16_t *>(base + L.xband_sidx) : nullptr;
     D.xband_seg = D.xcluster ? reinterpret_cast<const int32_t *>(base + L.xband_seg) : nullptr;

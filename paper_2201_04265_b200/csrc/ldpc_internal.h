@@ -40,7 +40,7 @@ struct DeviceLayout {
     // offsets into the owning CTA's message buffer (see spa_cluster.cu):
     size_t xband_ridx = 0; // uint16 [(wc-1)*n]  band edge (b>=1, p) -> slot in its row owner's buffer
     size_t xband_sidx = 0; // uint16 [n*(wc-1)]  variable v, band b>=1 -> slot in its variable owner's buffer
-    size_t xband_seg = 0;  // int32 [3][C C H (wc-1)] var-region offset, row-region offset, bytes per segment
+    size_t xband_seg = 0;  // int32 [3][C C H (wc-1) H] var-region offset, row-region offset, bytes per segment
     size_t total = 0;
 };
 
@@ -96,30 +96,34 @@ inline int xband_threads(int32_t mbq) {
     const int b0 = xband_rows_per_thread(mbq);
     return ((mbq + b0 - 1) / b0 + 31) / 32 * 32;
 }
-// Capacity (floats) of one message region: (wc-1) nq edge slots plus up to 3
-// floats of 16-byte padding per segment (H chunks x (wc-1) bands x C peers).
-inline int32_t xband_capacity(int32_t n, int32_t wc, int32_t wr, int32_t C) {
+// Region capacity (floats): (wc-1) nq edge slots plus the 16-byte padding of
+// its H x (wc-1) H x C segments -- worst case 3 floats each (shared-memory
+// sizing), expected 1.5 (cluster-size choice).  The exact capacity comes
+// from the tables at bind time (xband_tables); a code whose layout would
+// overflow the 16-bit byte slots gets no exchange view.
+inline int32_t xband_capacity_bound(int32_t n, int32_t wc, int32_t wr, int32_t C, int pad_x2 = 6) {
     const int32_t mbq = n / wr / C, nq = mbq * wr;
     const int32_t H = xband_rows_per_thread(mbq);
-    return ((wc - 1) * nq + 3 * H * (wc - 1) * C + 3) & ~3;
+    return ((wc - 1) * nq + (pad_x2 * H * H * (wc - 1) * C + 1) / 2 + 3) & ~3;
 }
-// Shared memory of the kernel: two regions + the CTA's two 16-bit slot tables
-// + barriers and flags.
-inline size_t xband_smem_bytes(int32_t n, int32_t wc, int32_t wr, int32_t C) {
-    const size_t nq = size_t(n / wr / C) * size_t(wr);
-    return 2 * size_t(xband_capacity(n, wc, wr, C)) * 4 + 2 * size_t(wc - 1) * nq * 2 + 16 + 8 * 16 + 4 * size_t(C);
+constexpr int32_t kXbandMaxCapacity = 16383;     // floats: byte slots < 65536
+// Shared memory of the kernel for region capacity `cap`: two regions + the
+// CTA's two 16-bit slot tables + barriers and flags.
+inline size_t xband_smem_bytes(int32_t n, int32_t wc, int32_t wr, int32_t C, int32_t cap) {
+    const size_t mbq = size_t(n / wr / C), nq = mbq * size_t(wr), H = size_t(xband_rows_per_thread(int32_t(mbq)));
+    return 2 * size_t(cap) * 4 + 2 * size_t(wc - 1) * nq * 2 + 16 + 8 * (2 + H + size_t(wc - 1) * H) + 4 * size_t(C);
 }
 // The smallest power of two C <= 16 with mb % C == 0 whose shared memory fits
-// one CTA and whose region offsets fit 16 bits; 0 when a frame fits one SM or
-// no such C exists.
+// one CTA and whose expected region fits 16-bit byte slots; 0 when a frame
+// fits one SM or no such C exists.
 inline int xband_cluster_size(int32_t n, int32_t wc, int32_t wr) {
     if (wc < 2 || wr < 1 || n % wr) return 0;
     if (size_t(wc) * size_t(n) * 4 + 1024 <= 227 * 1024) return 0;
     for (int C = 2; C <= 16; C *= 2) {
         if ((n / wr) % C) continue;
-        if (size_t(xband_capacity(n, wc, wr, C)) * 4 > 65532) continue;
+        if (xband_capacity_bound(n, wc, wr, C, 3) > kXbandMaxCapacity) continue;
         if (xband_threads(n / wr / C) + 32 > 1024) continue;      // + the producer warp
-        if (xband_smem_bytes(n, wc, wr, C) + 1024 <= 227 * 1024) return C;
+        if (xband_smem_bytes(n, wc, wr, C, xband_capacity_bound(n, wc, wr, C)) + 1024 <= 227 * 1024) return C;
     }
     return 0;
 }
@@ -153,8 +157,8 @@ struct ldpc_code {
 
 namespace ldpc {
 DeviceLayout compute_layout(const ldpc_code &c, bool with_G);
-void xband_tables(const ldpc_code &c, int C, std::vector<uint16_t> &ridx, std::vector<uint16_t> &sidx,
-                  std::vector<int32_t> &seg);
+int32_t xband_tables(const ldpc_code &c, int C, std::vector<uint16_t> &ridx, std::vector<uint16_t> &sidx,
+                     std::vector<int32_t> &seg);
 
 // Launch plan of the Gallager band kernel (spa_band.cu).
 struct BandPlan {

@@ -13,12 +13,12 @@
 // Message state lives IN PLACE in two shared-memory regions per CTA: every
 // band-b >= 1 edge has one slot in its variable owner's VAR region and one in
 // its row owner's ROW region (host_code.cpp xband_tables).
-//   C-phase: read L_vc from the ROW slot, write E_cv over it; after each band,
-//            ship that band's segments (one per (variable owner, V chunk)) to
-//            the owners' VAR regions.
+//   C-phase: read L_vc from the ROW slot, write E_cv over it; after each
+//            chunk (band, row step) ship its segments (one per (variable
+//            owner, V chunk)) to the owners' VAR regions.
 //   V-phase: read E_cv from the VAR slots, write L_vc over them; after each
-//            row chunk h, ship its segments (one per (band, row owner)) to the
-//            owners' ROW regions.
+//            row chunk h, ship its segments (one per (row owner, C chunk)) to
+//            the owners' ROW regions.
 // Shipping = cp.async.bulk shared::cta -> shared::cluster, complete_tx on the
 // receiver's region barrier, issued by a producer warp as soon as the compute
 // warps have arrived on the chunk's barrier: early chunks travel while later
@@ -144,7 +144,7 @@ __device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
 // Shared memory: VAR region | ROW region (cap floats each) | var slot table
 // u16 [nq][NB] | row slot table u16 [NB][mbq][WR] | barriers | flags[C].
 // Barriers: var_bar, row_bar (incoming E / L exchange, complete_tx),
-// vchunk[H], cchunk[NB] (compute warps finished a chunk).
+// vchunk[H], cchunk[NB H] (compute warps finished a chunk).
 // Warps: TW / 32 compute warps, then one producer warp that ships each chunk
 // as soon as every compute warp arrived on its chunk barrier -- no CTA-wide
 // barrier inside the iteration loop.
@@ -164,12 +164,13 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
     uint16_t *vtab = reinterpret_cast<uint16_t *>(smem + 2 * cap_b);
     uint16_t *rtab = vtab + size_t(nq) * NB;
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem + ((2 * cap_b + 4u * uint32_t(NB * nq) + 15u) & ~15u));
-    int *flags = reinterpret_cast<int *>(bars + 2 + H + NB);
+    constexpr int NC = NB * H;      // C-phase chunks: (band, row step)
+    int *flags = reinterpret_cast<int *>(bars + 2 + H + NC);
     const uint32_t var_s = saddr(varr), row_s = saddr(rowr), vbar = saddr(bars), rbar = vbar + 8;
     const uint32_t vchunk = vbar + 16, cchunk = vchunk + 8 * H;
-    const int nkey = C * C * H * NB;
+    const int nkey = C * C * H * NC;
     const int32_t *varOff = code.xband_seg, *rowOff = code.xband_seg + nkey, *sbytes = code.xband_seg + 2 * nkey;
-    auto key = [](int s, int d, int h, int b) { return ((s * C + d) * H + h) * NB + b; };
+    auto key = [](int s, int d, int h, int c) { return ((s * C + d) * H + h) * NC + c; };
 
     // slot tables of CTA q -> shared memory (once)
     {
@@ -186,15 +187,14 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
     uint32_t rx_l = 0, rx_e = 0;
     for (int s = 0; s < C; ++s)
         for (int h = 0; h < H; ++h)
-#pragma unroll
-            for (int b = 0; b < NB; ++b) {
-                rx_l += uint32_t(__ldg(sbytes + key(s, q, h, b)));
-                rx_e += uint32_t(__ldg(sbytes + key(q, s, h, b)));
+            for (int c = 0; c < NC; ++c) {
+                rx_l += uint32_t(__ldg(sbytes + key(s, q, h, c)));
+                rx_e += uint32_t(__ldg(sbytes + key(q, s, h, c)));
             }
     if (tt == 0) {
         mbar_init(vbar, 1);
         mbar_init(rbar, 1);
-        for (int i = 0; i < H + NB; ++i) mbar_init(vchunk + 8 * i, uint32_t(TW / 32));
+        for (int i = 0; i < H + NC; ++i) mbar_init(vchunk + 8 * i, uint32_t(TW / 32));
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         mbar_arm(vbar, rx_e);
         mbar_arm(rbar, rx_l);
@@ -209,24 +209,24 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
         if (lane == 0) mbar_arrive_local(bar);
     };
     uint32_t nv = 0, nc = 0;    // V / C phases shipped (producer: chunk barrier phases)
-    // producer: ship V chunk h (segments (q, d, h, b): VAR region -> ROW region of d)
+    // producer: ship V chunk h (segments (q, d, h, c): VAR region -> ROW region of d)
     auto ship_l = [&](int h) {
         mbar_wait(vchunk + 8 * h, nv & 1u);
-        if (lane < NB * C) {
-            const int b = lane / C, d = lane - b * C;
-            const int k = key(int(q), d, h, b);
+        for (int i = lane; i < C * NC; i += 32) {
+            const int d = i / NC, c = i - d * NC;
+            const int k = key(int(q), d, h, c);
             const uint32_t nbytes = uint32_t(__ldg(sbytes + k));
             if (nbytes)
                 bulk_s2c(mapa_u32(row_s + uint32_t(__ldg(rowOff + k)), uint32_t(d)), var_s + uint32_t(__ldg(varOff + k)),
                          nbytes, mapa_u32(rbar, uint32_t(d)));
         }
     };
-    // producer: ship C chunk b (segments (s, q, h, b): ROW region -> VAR region of s)
-    auto ship_e = [&](int b) {
-        mbar_wait(cchunk + 8 * b, nc & 1u);
+    // producer: ship C chunk c (segments (s, q, h, c): ROW region -> VAR region of s)
+    auto ship_e = [&](int c) {
+        mbar_wait(cchunk + 8 * c, nc & 1u);
         if (lane < C * H) {
             const int s = lane / H, h = lane - s * H;
-            const int k = key(s, int(q), h, b);
+            const int k = key(s, int(q), h, c);
             const uint32_t nbytes = uint32_t(__ldg(sbytes + k));
             if (nbytes)
                 bulk_s2c(mapa_u32(var_s + uint32_t(__ldg(varOff + k)), uint32_t(s)), row_s + uint32_t(__ldg(rowOff + k)),
@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
             ++nv;
             for (int t = 1; t <= a.max_iter; ++t) {
 #pragma unroll
-                for (int b = 0; b < NB; ++b) ship_e(b);
+                for (int c = 0; c < NC; ++c) ship_e(c);
                 ++nc;
 #pragma unroll
                 for (int h = 0; h < H; ++h) ship_l(h);
@@ -302,8 +302,8 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
 #pragma unroll
                             for (int j = 0; j < WR; ++j) *reinterpret_cast<float *>(rowr + sl[j]) = e[j];
                         }
+                        chunk_done(cchunk + 8 * (b * H + k));
                     }
-                    chunk_done(cchunk + 8 * b);
                 }
                 // ---- V-phase t (a4/a5): L = R + sum E; L_vc over the E slots (L itself at t = T)
                 const bool last = t == a.max_iter;
@@ -440,8 +440,8 @@ bool xcluster_plan(const ldpc_code &c, int64_t frames, bool et, XClusterPlan &p)
     p.kernel = k;
     p.cluster = C;
     p.threads = xband_threads(mbq) + 32;          // compute warps + the producer warp
-    if ((p.threads - 32) * H < mbq || (c.wc - 1) * C > 32 || C * H > 32) return false;
-    p.smem = xband_smem_bytes(c.n, c.wc, c.wr, C);
+    if ((p.threads - 32) * H < mbq || C * H > 32) return false;
+    p.smem = xband_smem_bytes(c.n, c.wc, c.wr, C, c.dev.xcap);
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p.smem)) != cudaSuccess) return false;
     if (C > 8 && cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) return false;
     cudaLaunchConfig_t cfg = {};
