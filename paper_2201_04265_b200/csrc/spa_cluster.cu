@@ -148,8 +148,9 @@ __device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
 // Warps: TW / 32 compute warps, then one producer warp that ships each chunk
 // as soon as every compute warp arrived on its chunk barrier -- no CTA-wide
 // barrier inside the iteration loop.
-template <int WR, int WC, int H, int C>
-__global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
+// MAXT: launch bound (768 lets a 736-thread C5 block keep 85 registers).
+template <int WR, int WC, int H, int C, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) xband_kernel(const XArgs a) {
     extern __shared__ __align__(128) char smem[];
     constexpr int NB = WC - 1;
     const DeviceCode &code = a.code;
@@ -264,24 +265,27 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
             }
         } else {
             // ---- V-phase 0 (a1/a2): L = R, E = 0; L_vc = R; band-0 check of t = 1
+            //      (after both chunks are handed to the producer, as below)
+            float lv[H][WR];
 #pragma unroll
             for (int h = 0; h < H; ++h) {
                 const int r = tt + h * TW;
                 if (r < mbq) {
                     const int v0 = (int(q) * mbq + r) * WR;
-                    float lv[WR];
-                    lds_row<WR>(reinterpret_cast<const char *>(llr), uint32_t(v0) * 4u, lv);   // global, 8B-aligned rows
+                    lds_row<WR>(reinterpret_cast<const char *>(llr), uint32_t(v0) * 4u, lv[h]);   // global, 8B-aligned rows
 #pragma unroll
-                    for (int j = 0; j < WR; ++j) lv[j] = fminf(fmaxf(lv[j], -30.0f), 30.0f) * kL2E;
+                    for (int j = 0; j < WR; ++j) lv[h][j] = fminf(fmaxf(lv[h][j], -30.0f), 30.0f) * kL2E;
                     const uint16_t *vt = vtab + size_t(r) * WR * NB;
 #pragma unroll
                     for (int j = 0; j < WR; ++j)
 #pragma unroll
-                        for (int b = 0; b < NB; ++b) *reinterpret_cast<float *>(varr + vt[j * NB + b]) = lv[j];
-                    check_row<WR, true>(lv, e0[h]);
+                        for (int b = 0; b < NB; ++b) *reinterpret_cast<float *>(varr + vt[j * NB + b]) = lv[h][j];
                 }
                 chunk_done(vchunk + 8 * h);
             }
+#pragma unroll
+            for (int h = 0; h < H; ++h)
+                if (tt + h * TW < mbq) check_row<WR, true>(lv[h], e0[h]);
             for (int t = 1; t <= a.max_iter; ++t) {
                 // ---- C-phase t (a3): rows of bands >= 1 owned by q, band by band
                 wait_row();
@@ -308,13 +312,14 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
                 // ---- V-phase t (a4/a5): L = R + sum E; L_vc over the E slots (L itself at t = T)
                 const bool last = t == a.max_iter;
                 wait_var();
+                // Each chunk's L_vc go to the producer first; the band-0 checks
+                // (thread-local, x = L - E0) run afterwards, overlapping the transfer.
 #pragma unroll
                 for (int h = 0; h < H; ++h) {
                     const int r = tt + h * TW;
                     if (r < mbq) {
                         const int v0 = (int(q) * mbq + r) * WR;
-                        float lv[WR];
-                        lds_row<WR>(reinterpret_cast<const char *>(llr), uint32_t(v0) * 4u, lv);
+                        lds_row<WR>(reinterpret_cast<const char *>(llr), uint32_t(v0) * 4u, lv[h]);
                         const uint16_t *vt = vtab + size_t(r) * WR * NB;
                         uint32_t sl[WR * NB];
 #pragma unroll
@@ -322,35 +327,38 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
                         float eb[WR * NB];
 #pragma unroll
                         for (int j = 0; j < WR; ++j) {
-                            lv[j] = fminf(fmaxf(lv[j], -30.0f), 30.0f) * kL2E + e0[h][j];
+                            lv[h][j] = fminf(fmaxf(lv[h][j], -30.0f), 30.0f) * kL2E + e0[h][j];
 #pragma unroll
                             for (int b = 0; b < NB; ++b) {
                                 eb[j * NB + b] = *reinterpret_cast<const float *>(varr + sl[j * NB + b]);
-                                lv[j] += eb[j * NB + b];
+                                lv[h][j] += eb[j * NB + b];
                             }
                         }
                         if (last) {
                             uint32_t rp = 0;      // band-0 row syndrome bit (Eq. 1)
 #pragma unroll
                             for (int j = 0; j < WR; ++j) {
-                                rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
+                                rp ^= (lv[h][j] >= 0.0f) ? 1u : 0u;
 #pragma unroll
-                                for (int b = 0; b < NB; ++b) *reinterpret_cast<float *>(varr + sl[j * NB + b]) = lv[j];
+                                for (int b = 0; b < NB; ++b) *reinterpret_cast<float *>(varr + sl[j * NB + b]) = lv[h][j];
                             }
                             synd |= rp;
                         } else {
-                            float x[WR];
 #pragma unroll
                             for (int j = 0; j < WR; ++j) {
 #pragma unroll
                                 for (int b = 0; b < NB; ++b)
-                                    *reinterpret_cast<float *>(varr + sl[j * NB + b]) = lv[j] - eb[j * NB + b];
-                                x[j] = lv[j] - e0[h][j];
+                                    *reinterpret_cast<float *>(varr + sl[j * NB + b]) = lv[h][j] - eb[j * NB + b];
+                                lv[h][j] -= e0[h][j];
                             }
-                            check_row<WR, true>(x, e0[h]);
                         }
                     }
                     chunk_done(vchunk + 8 * h);
+                }
+                if (!last) {
+#pragma unroll
+                    for (int h = 0; h < H; ++h)
+                        if (tt + h * TW < mbq) check_row<WR, true>(lv[h], e0[h]);
                 }
             }
             // ---- a7: syndrome of z = [L >= 0]: ROW slots now hold L (bands >= 1)
@@ -408,22 +416,22 @@ __global__ void __launch_bounds__(1024, 1) xband_kernel(const XArgs a) {
     }
 }
 
-template <int WR, int H>
+template <int WR, int H, int MAXT>
 void *pick_x_c(int C) {
     switch (C) {
-        case 4: return reinterpret_cast<void *>(&xband_kernel<WR, 3, H, 4>);
-        case 8: return reinterpret_cast<void *>(&xband_kernel<WR, 3, H, 8>);
-        case 16: return reinterpret_cast<void *>(&xband_kernel<WR, 3, H, 16>);
+        case 4: return reinterpret_cast<void *>(&xband_kernel<WR, 3, H, 4, MAXT>);
+        case 8: return reinterpret_cast<void *>(&xband_kernel<WR, 3, H, 8, MAXT>);
+        case 16: return reinterpret_cast<void *>(&xband_kernel<WR, 3, H, 16, MAXT>);
     }
     return nullptr;
 }
 
-void *pick_xband_kernel(int wr, int wc, int H, int C) {
+void *pick_xband_kernel(int wr, int wc, int H, int C, int threads) {
     if (wc != 3 || wr != 6) return nullptr;
     switch (H) {
-        case 1: return pick_x_c<6, 1>(C);
-        case 2: return pick_x_c<6, 2>(C);
-        case 4: return pick_x_c<6, 4>(C);
+        case 1: return pick_x_c<6, 1, 1024>(C);
+        case 2: return threads <= 768 ? pick_x_c<6, 2, 768>(C) : pick_x_c<6, 2, 1024>(C);
+        case 4: return pick_x_c<6, 4, 1024>(C);
     }
     return nullptr;
 }
@@ -435,11 +443,11 @@ bool xcluster_plan(const ldpc_code &c, int64_t frames, bool et, XClusterPlan &p)
     const int C = c.dev.xcluster;
     const int mbq = c.n / c.wr / C;
     const int H = xband_rows_per_thread(mbq);
-    void *k = pick_xband_kernel(c.wr, c.wc, H, C);
+    p.threads = xband_threads(mbq) + 32;          // compute warps + the producer warp
+    void *k = pick_xband_kernel(c.wr, c.wc, H, C, p.threads);
     if (!k) return false;
     p.kernel = k;
     p.cluster = C;
-    p.threads = xband_threads(mbq) + 32;          // compute warps + the producer warp
     if ((p.threads - 32) * H < mbq || C * H > 32) return false;
     p.smem = xband_smem_bytes(c.n, c.wc, c.wr, C, c.dev.xcap);
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p.smem)) != cudaSuccess) return false;
