@@ -37,6 +37,10 @@ import ldpc_workloads as W  # noqa: E402
 # edge per iteration, ex2 + lg2 each), 16 MUFU/clk/SM, 148 SMs.
 MUFU_PER_CLK_PER_SM = 16
 MUFU_PER_EDGE_UPDATE = 4
+KERNEL_NAMES = {1: "spa_decode_kernel (generic, on-chip)", 2: "spa_decode_kernel (generic, global state)",
+                3: "band_kernel (check-major E)", 4: "band_kernel (variable-major E)",
+                5: "band_cluster_kernel (L2 gathers)", 6: "band_kernel (variable-major E, 16-bit offsets)",
+                7: "xband_kernel (exchange cluster, bulk DSMEM segments)"}
 
 
 def parse():
@@ -357,9 +361,10 @@ def main():
     clock_mhz = measured_peaks().get("sm_max_mhz", 1965.0)
     peak = sms * MUFU_PER_CLK_PER_SM * clock_mhz * 1e6 / MUFU_PER_EDGE_UPDATE / 1e9
     clocks = clk.summary()
+    variant = L.ldpc_decode_variant(code, frames, wl.max_iter, wl.early_term, args.variant)
 
     # ---- end to end through the public API with host buffers (rank-local)
-    e2e = e2e_measure(L, code, wl, args, dev, frame0, k, n, kw, nw, world)
+    e2e = e2e_measure(L, code, wl, args, dev, frame0, k, n, kw, nw, world, frames)
 
     # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
@@ -383,7 +388,7 @@ def main():
             "mean_iterations": iters_mean, "k": k,
             "counters": {"info_bit_errors": int(ctr[0]), "cw_bit_errors": int(ctr[1]),
                          "frame_errors": int(ctr[2]), "undetected": int(ctr[3]), "frames": int(ctr[5])},
-            "roofline": {"bound": "alu", "kernel": "ldpc_decode (band_kernel for Gallager codes)",
+            "roofline": {"bound": "alu", "kernel": f"ldpc_decode variant {variant}: {KERNEL_NAMES.get(variant, '?')}",
                          "achieved": achieved, "peak": peak,
                          "unit": "Gedge-updates/s", "frac": achieved / peak, "traffic": dram_traffic(wl, frames),
                          "peak_basis": f"SFU: {sms} SMs x 16 MUFU/clk x {clock_mhz:.0f} MHz / 4 MUFU per "
@@ -401,12 +406,13 @@ def main():
     return 0
 
 
-def e2e_measure(L, code, wl, args, dev, frame0, k, n, kw, nw, world):
+def e2e_measure(L, code, wl, args, dev, frame0, k, n, kw, nw, world, frames):
     """Same metric through the public API with pinned host buffers: H2D of the
     step's info bits and LLRs, encode, decode, count, D2H of the decoded bits
-    and the counters, all inside the timed region."""
+    and the counters, all inside the timed region.  The step is the device
+    arm's batch (`frames`)."""
     import torch
-    F = args.frames or wl.frames
+    F = frames
     if args.e2e_frames:
         F = min(F, args.e2e_frames)
     Fc = min(F, 16384)                       # pipeline chunk
