@@ -2,6 +2,11 @@
 // external CSR), standard-form generator (GF(2) Gauss-Jordan), queries, the
 // device image, and the frame partition.  Independent of oracle/ (shares no
 // code with it); bit-exactness with it is asserted by tests/test_host_vs_oracle.py.
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -74,6 +79,97 @@ unsigned worker_count() {
 }  // namespace
 
 namespace ldpc {
+namespace {
+std::mutex g_launch_mu;
+std::map<std::pair<int, int>, int> g_dev_attr;                                   // (device, attr)
+std::map<std::pair<int, const void *>, size_t> g_smem_attr;                       // (device, kernel)
+std::map<std::tuple<int, const void *, int, size_t, int>, int> g_occupancy;      // (device, kernel, T, smem, C)
+int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+}  // namespace
+
+int device_attribute(int attr) {
+    const int d = current_device();
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    auto it = g_dev_attr.find({d, attr});
+    if (it != g_dev_attr.end()) return it->second;
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, static_cast<cudaDeviceAttr>(attr), d) != cudaSuccess) return -1;
+    g_dev_attr[{d, attr}] = v;
+    return v;
+}
+
+bool ensure_smem_attribute(const void *kernel, size_t smem, bool nonportable_cluster) {
+    const int d = current_device();
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    size_t &have = g_smem_attr[{d, kernel}];
+    if (have >= smem && have > 0) return true;
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(std::max(smem, have))) !=
+        cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    if (nonportable_cluster && cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                                   cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    have = std::max(smem, std::max<size_t>(have, 1));
+    return true;
+}
+
+int occupancy_blocks(const void *kernel, int threads, size_t smem) {
+    const int d = current_device();
+    {
+        std::lock_guard<std::mutex> lk(g_launch_mu);
+        auto it = g_occupancy.find({d, kernel, threads, smem, 0});
+        if (it != g_occupancy.end()) return it->second;
+    }
+    int v = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kernel, threads, smem) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    g_occupancy[{d, kernel, threads, smem, 0}] = v;
+    return v;
+}
+
+int occupancy_clusters(const void *kernel, int threads, size_t smem, int cluster) {
+    const int d = current_device();
+    {
+        std::lock_guard<std::mutex> lk(g_launch_mu);
+        auto it = g_occupancy.find({d, kernel, threads, smem, cluster});
+        if (it != g_occupancy.end()) return it->second;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(cluster);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(unsigned(cluster));
+    cfg.blockDim = dim3(unsigned(threads));
+    cfg.dynamicSmemBytes = smem;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int v = 0;
+    const cudaError_t e = cudaOccupancyMaxActiveClusters(&v, kernel, &cfg);
+    if (e != cudaSuccess) {
+        if (std::getenv("LDPC_DEBUG"))
+            std::fprintf(stderr, "ldpc occupancy_clusters: %s (C=%d, threads %d, smem %zu)\n", cudaGetErrorString(e),
+                         cluster, threads, smem);
+        cudaGetLastError();
+        return -1;
+    }
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    g_occupancy[{d, kernel, threads, smem, cluster}] = v;
+    return v;
+}
+
 DeviceLayout compute_layout(const ldpc_code &c, bool with_G) {
     DeviceLayout L;
     size_t off = 0;

@@ -156,6 +156,15 @@ struct ldpc_code {
 };
 
 namespace ldpc {
+// Launch-configuration queries, cached per (device, kernel, block size,
+// dynamic smem[, cluster size]) so that repeated ldpc_decode calls (stream
+// mode issues one per frame) make no driver queries.  The dynamic
+// shared-memory attribute of a kernel is only ever raised.  -1 on failure.
+int device_attribute(int attr);                       // cudaDeviceAttr of the current device
+bool ensure_smem_attribute(const void *kernel, size_t smem, bool nonportable_cluster = false);
+int occupancy_blocks(const void *kernel, int threads, size_t smem);
+int occupancy_clusters(const void *kernel, int threads, size_t smem, int cluster);
+
 DeviceLayout compute_layout(const ldpc_code &c, bool with_G);
 int32_t xband_tables(const ldpc_code &c, int C, std::vector<uint16_t> &ridx, std::vector<uint16_t> &sidx,
                      std::vector<int32_t> &seg);

@@ -490,40 +490,17 @@ bool cluster_plan(const ldpc_code &c, int64_t frames, bool et, ClusterPlan &p) {
     const int b0 = std::max(1, (mbq + 1023) / 1024);
     void *k = pick_cluster_kernel(c.wr, c.wc, b0, C);
     if (!k) return false;
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     p.kernel = k;
     p.cluster = C;
     p.threads = ((mbq + b0 - 1) / b0 + 31) / 32 * 32;
     p.smem = size_t(c.wc) * size_t(nq) * 4;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p.smem)) != cudaSuccess) return false;
-    if (C > 8 && cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) return false;
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = unsigned(C);
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(unsigned(C));
-    cfg.blockDim = dim3(unsigned(p.threads));
-    cfg.dynamicSmemBytes = p.smem;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int nclusters = 0;
-    const cudaError_t oe = cudaOccupancyMaxActiveClusters(&nclusters, k, &cfg);
-    if (oe != cudaSuccess || nclusters < 1) {
-        if (std::getenv("LDPC_DEBUG"))
-            std::fprintf(stderr, "ldpc cluster_plan: occupancy query: %s, clusters %d (C=%d, threads %d, smem %zu)\n",
-                         cudaGetErrorString(oe), nclusters, C, p.threads, p.smem);
-        cudaGetLastError();
-        return false;
-    }
+    if (!ensure_smem_attribute(k, p.smem, C > 8)) return false;
+    int nclusters = occupancy_clusters(k, p.threads, p.smem, C);
+    if (nclusters < 1) return false;
     nclusters = int(std::min<int64_t>(nclusters, std::max<int64_t>(frames, 1)));
     p.grid = nclusters * C;
     p.slot_floats = (int64_t(c.wc + 1) * c.n + 16 + 63) & ~int64_t(63);
     p.ws_bytes = size_t(nclusters) * size_t(p.slot_floats) * 4;
-    (void)sms;
     return true;
 }
 
@@ -562,10 +539,9 @@ ldpc_status cluster_launch(const ldpc_code &c, const ClusterPlan &p, const float
 bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPlan &p) {
     if (!c.gallager || !c.regular_col || (c.n & 3)) return false;
     const int mb = c.n / c.wr;
-    int dev = 0, sms = 0, optin = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const int sms = device_attribute(cudaDevAttrMultiProcessorCount);
+    const int optin = device_attribute(cudaDevAttrMaxSharedMemoryPerBlockOptin);
+    if (sms < 1 || optin < 1) return false;
     const int b0 = std::max(1, (mb + 1023) / 1024);
     if (b0 > 4) return false;
     const size_t base = size_t(c.wc) * size_t(c.n) * 4;          // E_hi + L
@@ -580,16 +556,13 @@ bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPla
     p.mode = p.vm ? (((variant == 6 || variant == 0) && c.n <= 16383) ? 2 : 1) : 0;
     void *k = pick_band_kernel(c.wr, c.wc, b0, et, p.mode);
     if (!k) return false;
-    cudaFuncAttributes fa;
-    if (cudaFuncGetAttributes(&fa, k) != cudaSuccess) return false;
-    if (((mb + b0 - 1) / b0 + 31) / 32 * 32 > fa.maxThreadsPerBlock) return false;
     p.smem = p.r_in_smem ? with_r : base;
     p.threads = ((mb + b0 - 1) / b0 + 31) / 32 * 32;
+    if (p.threads > (c.wc > 3 ? 256 : 1024)) return false;        // the kernel's launch bound
     p.kernel = k;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p.smem)) != cudaSuccess) return false;
-    int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, p.threads, p.smem) != cudaSuccess || per_sm < 1)
-        return false;
+    if (!ensure_smem_attribute(k, p.smem)) return false;
+    const int per_sm = occupancy_blocks(k, p.threads, p.smem);
+    if (per_sm < 1) return false;
     p.grid = int(std::max<int64_t>(1, std::min<int64_t>(frames, int64_t(sms) * per_sm)));
     p.ws_bytes = 256 + (p.r_in_smem ? 0 : size_t(p.grid) * size_t(c.n) * 4);
     return true;

@@ -450,28 +450,9 @@ bool xcluster_plan(const ldpc_code &c, int64_t frames, bool et, XClusterPlan &p)
     p.cluster = C;
     if ((p.threads - 32) * H < mbq || C * H > 32) return false;
     p.smem = xband_smem_bytes(c.n, c.wc, c.wr, C, c.dev.xcap);
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p.smem)) != cudaSuccess) return false;
-    if (C > 8 && cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) return false;
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = unsigned(C);
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(unsigned(C));
-    cfg.blockDim = dim3(unsigned(p.threads));
-    cfg.dynamicSmemBytes = p.smem;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int nclusters = 0;
-    const cudaError_t oe = cudaOccupancyMaxActiveClusters(&nclusters, k, &cfg);
-    if (oe != cudaSuccess || nclusters < 1) {
-        if (std::getenv("LDPC_DEBUG"))
-            std::fprintf(stderr, "ldpc xcluster_plan: occupancy query: %s, clusters %d (C=%d, threads %d, smem %zu)\n",
-                         cudaGetErrorString(oe), nclusters, C, p.threads, p.smem);
-        cudaGetLastError();
-        return false;
-    }
+    if (!ensure_smem_attribute(k, p.smem, C > 8)) return false;
+    int nclusters = occupancy_clusters(k, p.threads, p.smem, C);
+    if (nclusters < 1) return false;
     nclusters = int(std::min<int64_t>(nclusters, std::max<int64_t>(frames, 1)));
     p.grid = nclusters * C;
     p.ws_bytes = 0;

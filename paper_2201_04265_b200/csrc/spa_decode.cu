@@ -406,12 +406,8 @@ struct DeviceProps {
 };
 DeviceProps device_props() {
     DeviceProps p;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&p.sms, cudaDevAttrMultiProcessorCount, dev);
-    int v = 0;
-    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    p.smem_optin = size_t(v);
+    p.sms = device_attribute(cudaDevAttrMultiProcessorCount);
+    p.smem_optin = size_t(std::max(device_attribute(cudaDevAttrMaxSharedMemoryPerBlockOptin), 0));
     return p;
 }
 
@@ -444,11 +440,9 @@ ldpc_status make_plan(const ldpc_code &c, int64_t frames, const ldpc_decode_opts
         p.team_threads = T;
         p.teams_per_cta = teams;
         p.smem_bytes = per_team_bytes * size_t(teams);
-        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p.smem_bytes)) != cudaSuccess)
-            return LDPC_ERR_CUDA;
-        int blocks_per_sm = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k, T * teams, p.smem_bytes) != cudaSuccess)
-            return LDPC_ERR_CUDA;
+        if (!ensure_smem_attribute(k, p.smem_bytes)) return LDPC_ERR_CUDA;
+        int blocks_per_sm = occupancy_blocks(k, T * teams, p.smem_bytes);
+        if (blocks_per_sm < 0) return LDPC_ERR_CUDA;
         blocks_per_sm = std::max(blocks_per_sm, 1);
         const int64_t want = (frames + teams - 1) / teams;
         p.grid = int(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(dp.sms) * blocks_per_sm)));
@@ -458,9 +452,8 @@ ldpc_status make_plan(const ldpc_code &c, int64_t frames, const ldpc_decode_opts
         p.team_threads = 1024;
         p.teams_per_cta = 1;
         p.smem_bytes = 0;
-        int blocks_per_sm = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k, 1024, 0) != cudaSuccess)
-            return LDPC_ERR_CUDA;
+        int blocks_per_sm = occupancy_blocks(k, 1024, 0);
+        if (blocks_per_sm < 0) return LDPC_ERR_CUDA;
         blocks_per_sm = std::max(blocks_per_sm, 1);
         p.grid = int(std::max<int64_t>(1, std::min<int64_t>(frames, int64_t(dp.sms) * blocks_per_sm)));
         p.ws_stride = per_team_floats;
