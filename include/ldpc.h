@@ -161,7 +161,11 @@ ldpc_status ldpc_decode_workspace_bytes(const ldpc_code *code, int64_t frames,
  * remote messages through L2-resident global copies); 6 = 4 with 16-bit
  * offsets (n <= 16383); 7 exchange cluster kernel (same codes as 5; a
  * cluster of C CTAs per frame trades message segments with bulk DSMEM copies,
- * no workspace; preferred by auto). */
+ * no workspace; fixed iterations, wr = 6).  Auto (0): a frame that fits one SM
+ * runs the band kernel (one SM per frame) unless the batch is too small to
+ * fill the GPU that way, in which case it runs variant 7 with C SMs per frame
+ * (lower latency: stream mode, small batches); larger frames run 7, else 5;
+ * any other H runs 1 or 2. */
 ldpc_status ldpc_decode(const ldpc_code *code, const float *d_llr, int64_t frames,
                         const ldpc_decode_opts *opts, uint32_t *d_bits,
                         uint8_t *d_syndrome_ok, int32_t *d_iters, float *d_posterior,

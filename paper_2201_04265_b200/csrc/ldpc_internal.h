@@ -113,18 +113,27 @@ inline size_t xband_smem_bytes(int32_t n, int32_t wc, int32_t wr, int32_t C, int
     const size_t mbq = size_t(n / wr / C), nq = mbq * size_t(wr), H = size_t(xband_rows_per_thread(int32_t(mbq)));
     return 2 * size_t(cap) * 4 + 2 * size_t(wc - 1) * nq * 2 + 16 + 8 * (2 + H + size_t(wc - 1) * H) + 4 * size_t(C);
 }
-// The smallest power of two C <= 16 with mb % C == 0 whose shared memory fits
-// one CTA and whose expected region fits 16-bit byte slots; 0 when a frame
-// fits one SM or no such C exists.
+// Cluster size of a code's exchange view.  Frames larger than one SM: the
+// smallest power of two C <= 16 with mb % C == 0 whose shared memory fits one
+// CTA and whose expected region fits 16-bit byte slots (throughput: C5 -> 8).
+// Frames that fit one SM: the largest C in {8, 4, 2} with >= 64 rows per CTA
+// (latency: stream mode and small batches, C4 -> 4).  0: no view.
+inline bool xband_fits(int32_t n, int32_t wc, int32_t wr, int C) {
+    if ((n / wr) % C) return false;
+    if (xband_capacity_bound(n, wc, wr, C, 3) > kXbandMaxCapacity) return false;
+    if (xband_threads(n / wr / C) + 32 > 1024) return false;      // + the producer warp
+    return xband_smem_bytes(n, wc, wr, C, xband_capacity_bound(n, wc, wr, C)) + 1024 <= 227 * 1024;
+}
+inline bool band_frame_fits_sm(int32_t n, int32_t wc) { return size_t(wc) * size_t(n) * 4 + 1024 <= 227 * 1024; }
 inline int xband_cluster_size(int32_t n, int32_t wc, int32_t wr) {
     if (wc < 2 || wr < 1 || n % wr) return 0;
-    if (size_t(wc) * size_t(n) * 4 + 1024 <= 227 * 1024) return 0;
-    for (int C = 2; C <= 16; C *= 2) {
-        if ((n / wr) % C) continue;
-        if (xband_capacity_bound(n, wc, wr, C, 3) > kXbandMaxCapacity) continue;
-        if (xband_threads(n / wr / C) + 32 > 1024) continue;      // + the producer warp
-        if (xband_smem_bytes(n, wc, wr, C, xband_capacity_bound(n, wc, wr, C)) + 1024 <= 227 * 1024) return C;
+    if (band_frame_fits_sm(n, wc)) {
+        for (int C = 8; C >= 2; C /= 2)
+            if ((n / wr) % C == 0 && n / wr / C >= 64 && xband_fits(n, wc, wr, C)) return C;
+        return 0;
     }
+    for (int C = 2; C <= 16; C *= 2)
+        if (xband_fits(n, wc, wr, C)) return C;
     return 0;
 }
 
@@ -174,6 +183,7 @@ struct BandPlan {
     void *kernel = nullptr;
     int threads = 0;
     int grid = 0;
+    int64_t capacity = 0;       // frames decoded concurrently (SMs x CTAs per SM)
     size_t smem = 0;
     bool r_in_smem = false;
     bool vm = false;            // E of bands >= 1 stored variable-major
@@ -206,6 +216,7 @@ struct XClusterPlan {
     int cluster = 0;
     int threads = 0;
     int grid = 0;
+    int64_t capacity = 0;       // frames decoded concurrently (co-resident clusters)
     size_t smem = 0;
     size_t ws_bytes = 0;
 };

@@ -563,7 +563,8 @@ bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPla
     if (!ensure_smem_attribute(k, p.smem)) return false;
     const int per_sm = occupancy_blocks(k, p.threads, p.smem);
     if (per_sm < 1) return false;
-    p.grid = int(std::max<int64_t>(1, std::min<int64_t>(frames, int64_t(sms) * per_sm)));
+    p.capacity = int64_t(sms) * per_sm;
+    p.grid = int(std::max<int64_t>(1, std::min<int64_t>(frames, p.capacity)));
     p.ws_bytes = 256 + (p.r_in_smem ? 0 : size_t(p.grid) * size_t(c.n) * 4);
     return true;
 }

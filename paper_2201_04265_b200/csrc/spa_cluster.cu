@@ -419,6 +419,7 @@ __global__ void __launch_bounds__(MAXT, 1) xband_kernel(const XArgs a) {
 template <int WR, int H, int MAXT>
 void *pick_x_c(int C) {
     switch (C) {
+        case 2: return reinterpret_cast<void *>(&xband_kernel<WR, 3, H, 2, MAXT>);
         case 4: return reinterpret_cast<void *>(&xband_kernel<WR, 3, H, 4, MAXT>);
         case 8: return reinterpret_cast<void *>(&xband_kernel<WR, 3, H, 8, MAXT>);
         case 16: return reinterpret_cast<void *>(&xband_kernel<WR, 3, H, 16, MAXT>);
@@ -429,7 +430,7 @@ void *pick_x_c(int C) {
 void *pick_xband_kernel(int wr, int wc, int H, int C, int threads) {
     if (wc != 3 || wr != 6) return nullptr;
     switch (H) {
-        case 1: return pick_x_c<6, 1, 1024>(C);
+        case 1: return threads <= 768 ? pick_x_c<6, 1, 768>(C) : pick_x_c<6, 1, 1024>(C);
         case 2: return threads <= 768 ? pick_x_c<6, 2, 768>(C) : pick_x_c<6, 2, 1024>(C);
         case 4: return pick_x_c<6, 4, 1024>(C);
     }
@@ -453,6 +454,7 @@ bool xcluster_plan(const ldpc_code &c, int64_t frames, bool et, XClusterPlan &p)
     if (!ensure_smem_attribute(k, p.smem, C > 8)) return false;
     int nclusters = occupancy_clusters(k, p.threads, p.smem, C);
     if (nclusters < 1) return false;
+    p.capacity = nclusters;
     nclusters = int(std::min<int64_t>(nclusters, std::max<int64_t>(frames, 1)));
     p.grid = nclusters * C;
     p.ws_bytes = 0;

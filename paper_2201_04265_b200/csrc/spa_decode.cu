@@ -465,75 +465,96 @@ ldpc_status make_plan(const ldpc_code &c, int64_t frames, const ldpc_decode_opts
 }  // namespace
 }  // namespace ldpc
 
+namespace ldpc {
+namespace {
+// The decoder ldpc_decode runs (opts->variant 0 resolved) and its plan.
+// Auto order: the Gallager band kernel when a frame fits one SM -- unless the
+// batch is too small to fill the GPU one frame per SM and the code has an
+// exchange (cluster) view, which then decodes each frame on C SMs for lower
+// latency; the exchange cluster kernel for frames larger than one SM (else
+// the L2-gather cluster kernel); the generic CSR kernels otherwise.
+struct Resolved {
+    int variant = 0;
+    BandPlan band;
+    XClusterPlan x;
+    ClusterPlan cl;
+    Plan gen;
+};
+ldpc_status resolve(const ldpc_code &c, int64_t frames, const ldpc_decode_opts &o, Resolved &r) {
+    const int v = o.variant;
+    const bool et = o.early_term != 0;
+    frames = std::max<int64_t>(frames, 1);
+    const bool want_band = v == 0 || v == 3 || v == 4 || v == 6;
+    const bool band_ok = want_band && band_plan(c, frames, et, v, r.band);
+    if (want_band && v != 0) {
+        if (!band_ok) return LDPC_ERR_UNSUPPORTED;
+        r.variant = r.band.mode == 2 ? 6 : (r.band.vm ? 4 : 3);
+        return LDPC_OK;
+    }
+    const bool x_ok = (v == 0 || v == 7) && xcluster_plan(c, frames, et, r.x);
+    if (v == 7) {
+        if (!x_ok) return LDPC_ERR_UNSUPPORTED;
+        r.variant = 7;
+        return LDPC_OK;
+    }
+    if (band_ok) {
+        // rounds of the one-SM-per-frame kernel vs rounds of C-SM clusters, a
+        // cluster round costing ~2/C of a band round (measured per-SM rate of
+        // the exchange kernel is about half the band kernel's)
+        if (x_ok) {
+            const int64_t rb = (frames + r.band.capacity - 1) / r.band.capacity;
+            const int64_t rx = (frames + r.x.capacity - 1) / r.x.capacity;
+            if (rx * 2 < rb * r.x.cluster) {
+                r.variant = 7;
+                return LDPC_OK;
+            }
+        }
+        r.variant = r.band.mode == 2 ? 6 : (r.band.vm ? 4 : 3);
+        return LDPC_OK;
+    }
+    if (x_ok) {
+        r.variant = 7;
+        return LDPC_OK;
+    }
+    if (v == 0 || v == 5) {
+        if (cluster_plan(c, frames, et, r.cl)) {
+            r.variant = 5;
+            return LDPC_OK;
+        }
+        if (v == 5) return LDPC_ERR_UNSUPPORTED;
+    }
+    const ldpc_status s = make_plan(c, frames, o, r.gen);
+    if (s != LDPC_OK) return s;
+    r.variant = r.gen.variant;
+    return LDPC_OK;
+}
+}  // namespace
+}  // namespace ldpc
+
 extern "C" {
 
 ldpc_status ldpc_decode_variant(const ldpc_code *code, int64_t frames, const ldpc_decode_opts *opts,
                                 int32_t *variant) {
     if (!code || !opts || !variant || frames < 0) return LDPC_ERR_ARG;
     *variant = 0;
-    frames = std::max<int64_t>(frames, 1);
-    if (opts->variant == 0 || opts->variant == 3 || opts->variant == 4 || opts->variant == 6) {
-        ldpc::BandPlan bp;
-        if (ldpc::band_plan(*code, frames, opts->early_term != 0, opts->variant, bp)) {
-            *variant = bp.mode == 2 ? 6 : (bp.vm ? 4 : 3);
-            return LDPC_OK;
-        }
-        if (opts->variant != 0) return LDPC_ERR_UNSUPPORTED;
-    }
-    if (opts->variant == 0 || opts->variant == 7) {
-        ldpc::XClusterPlan xp;
-        if (ldpc::xcluster_plan(*code, frames, opts->early_term != 0, xp)) {
-            *variant = 7;
-            return LDPC_OK;
-        }
-        if (opts->variant == 7) return LDPC_ERR_UNSUPPORTED;
-    }
-    if (opts->variant == 0 || opts->variant == 5) {
-        ldpc::ClusterPlan cp;
-        if (ldpc::cluster_plan(*code, frames, opts->early_term != 0, cp)) {
-            *variant = 5;
-            return LDPC_OK;
-        }
-        if (opts->variant == 5) return LDPC_ERR_UNSUPPORTED;
-    }
-    ldpc::Plan p;
-    ldpc_status s = ldpc::make_plan(*code, frames, *opts, p);
-    if (s != LDPC_OK) return s;
-    *variant = p.variant;
-    return LDPC_OK;
+    ldpc::Resolved r;
+    const ldpc_status s = ldpc::resolve(*code, frames, *opts, r);
+    if (s == LDPC_OK) *variant = r.variant;
+    return s;
 }
 
 ldpc_status ldpc_decode_workspace_bytes(const ldpc_code *code, int64_t frames, const ldpc_decode_opts *opts,
                                         size_t *bytes) {
     if (!code || !opts || !bytes || frames < 0) return LDPC_ERR_ARG;
-    if (opts->variant == 0 || opts->variant == 3 || opts->variant == 4 || opts->variant == 6) {
-        ldpc::BandPlan bp;
-        if (ldpc::band_plan(*code, std::max<int64_t>(frames, 1), opts->early_term != 0, opts->variant, bp)) {
-            *bytes = bp.ws_bytes;
-            return LDPC_OK;
-        }
-        if (opts->variant != 0) return LDPC_ERR_UNSUPPORTED;
-    }
-    if (opts->variant == 0 || opts->variant == 7) {
-        ldpc::XClusterPlan xp;
-        if (ldpc::xcluster_plan(*code, std::max<int64_t>(frames, 1), opts->early_term != 0, xp)) {
-            *bytes = xp.ws_bytes;
-            return LDPC_OK;
-        }
-        if (opts->variant == 7) return LDPC_ERR_UNSUPPORTED;
-    }
-    if (opts->variant == 0 || opts->variant == 5) {
-        ldpc::ClusterPlan cp;
-        if (ldpc::cluster_plan(*code, std::max<int64_t>(frames, 1), opts->early_term != 0, cp)) {
-            *bytes = cp.ws_bytes;
-            return LDPC_OK;
-        }
-        if (opts->variant == 5) return LDPC_ERR_UNSUPPORTED;
-    }
-    ldpc::Plan p;
-    ldpc_status s = ldpc::make_plan(*code, std::max<int64_t>(frames, 1), *opts, p);
+    ldpc::Resolved r;
+    const ldpc_status s = ldpc::resolve(*code, frames, *opts, r);
     if (s != LDPC_OK) return s;
-    *bytes = p.ws_bytes;
+    switch (r.variant) {
+        case 3: case 4: case 6: *bytes = r.band.ws_bytes; break;
+        case 7: *bytes = r.x.ws_bytes; break;
+        case 5: *bytes = r.cl.ws_bytes; break;
+        default: *bytes = r.gen.ws_bytes; break;
+    }
     return LDPC_OK;
 }
 
@@ -546,30 +567,22 @@ ldpc_status ldpc_decode(const ldpc_code *code, const float *d_llr, int64_t frame
     if (frames == 0) return LDPC_OK;
     if (!d_llr || !d_bits || !d_syndrome_ok || !d_iters) return LDPC_ERR_ARG;
     if (reinterpret_cast<uintptr_t>(d_llr) & 15u) return LDPC_ERR_ARG;
-    if (opts->variant == 0 || opts->variant == 3 || opts->variant == 4 || opts->variant == 6) {
-        ldpc::BandPlan bp;
-        if (ldpc::band_plan(*code, frames, opts->early_term != 0, opts->variant, bp))
-            return ldpc::band_launch(*code, bp, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters, d_posterior,
+    ldpc::Resolved r;
+    const ldpc_status rs = ldpc::resolve(*code, frames, *opts, r);
+    if (rs != LDPC_OK) return rs;
+    switch (r.variant) {
+        case 3: case 4: case 6:
+            return ldpc::band_launch(*code, r.band, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters, d_posterior,
                                      d_ws, ws_bytes, stream);
-        if (opts->variant != 0) return LDPC_ERR_UNSUPPORTED;
-    }
-    if (opts->variant == 0 || opts->variant == 7) {
-        ldpc::XClusterPlan xp;
-        if (ldpc::xcluster_plan(*code, frames, opts->early_term != 0, xp))
-            return ldpc::xcluster_launch(*code, xp, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters,
+        case 7:
+            return ldpc::xcluster_launch(*code, r.x, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters,
                                          d_posterior, stream);
-        if (opts->variant == 7) return LDPC_ERR_UNSUPPORTED;
-    }
-    if (opts->variant == 0 || opts->variant == 5) {
-        ldpc::ClusterPlan cp;
-        if (ldpc::cluster_plan(*code, frames, opts->early_term != 0, cp))
-            return ldpc::cluster_launch(*code, cp, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters,
+        case 5:
+            return ldpc::cluster_launch(*code, r.cl, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters,
                                         d_posterior, d_ws, ws_bytes, stream);
-        if (opts->variant == 5) return LDPC_ERR_UNSUPPORTED;
+        default: break;
     }
-    ldpc::Plan p;
-    ldpc_status s = ldpc::make_plan(*code, frames, *opts, p);
-    if (s != LDPC_OK) return s;
+    const ldpc::Plan &p = r.gen;
     if (p.ws_bytes > 0 && (!d_ws || ws_bytes < p.ws_bytes)) return LDPC_ERR_ARG;
     ldpc::DecodeArgs a;
     a.code = code->dev;
