@@ -90,6 +90,20 @@ ldpc_status ldpc_make_H(int32_t n, int32_t wc, int32_t wr, uint64_t seed, ldpc_c
 ldpc_status ldpc_code_from_csr(int32_t m, int32_t n, const int32_t *row_ptr,
                                const int32_t *col_idx, ldpc_code **out);
 
+/* MacKay alist text (P:4): "n m", "max_col_weight
+ * max_row_weight", the n column weights, the m row weights, n lines of 1-based
+ * row indices per column and m lines of 1-based column indices per row, each
+ * zero-padded to the maximum weight ('\n' line ends).
+ * write: *len = text length (excluding the NUL).  buf == NULL only queries
+ *   *len; otherwise cap must be >= *len + 1 (else LDPC_ERR_DIM).  Index lists
+ *   are written in ascending order.
+ * from_alist: text[len] (host, not NUL-terminated necessarily); the row lists
+ *   define H (rows kept in file order), the column lists must describe the same
+ *   matrix and every weight must match (LDPC_ERR_DIM); malformed text
+ *   LDPC_ERR_ARG; then as ldpc_code_from_csr. */
+ldpc_status ldpc_code_write_alist(const ldpc_code *code, char *buf, size_t cap, size_t *len);
+ldpc_status ldpc_code_from_alist(const char *text, size_t len, ldpc_code **out);
+
 /* Generator in standard form (Eq. 2-3): Gauss-Jordan
  * elimination of H over GF(2), columns scanned right to left, pivot = lowest
  * row index >= r (reading Q13).  Sets rank, k = n - rank, perm = [free

@@ -89,6 +89,23 @@ def ldpc_code_from_csr(m: int, n: int, row_ptr, col_idx) -> Code:
     return Code(h)
 
 
+def ldpc_code_from_alist(text) -> Code:
+    """MacKay alist text (str or bytes) -> code."""
+    b = text.encode() if isinstance(text, str) else bytes(text)
+    h = C.c_void_p()
+    call("ldpc_code_from_alist", C.c_char_p(b), C.c_size_t(len(b)), C.byref(h))
+    return Code(h)
+
+
+def ldpc_code_write_alist(code: Code) -> str:
+    """Code -> MacKay alist text."""
+    n = C.c_size_t(0)
+    call("ldpc_code_write_alist", code.handle, None, C.c_size_t(0), C.byref(n))
+    buf = C.create_string_buffer(n.value + 1)
+    call("ldpc_code_write_alist", code.handle, buf, C.c_size_t(n.value + 1), C.byref(n))
+    return buf.raw[:n.value].decode()
+
+
 def ldpc_make_G(code: Code) -> Code:
     call("ldpc_make_G", code.handle)
     return code

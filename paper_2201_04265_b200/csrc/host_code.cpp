@@ -13,6 +13,7 @@
 #include <cstring>
 #include <new>
 #include <thread>
+#include <string>
 #include <vector>
 
 #include "ldpc_internal.h"
@@ -367,6 +368,133 @@ ldpc_status ldpc_code_from_csr(int32_t m, int32_t n, const int32_t *row_ptr, con
     }
     *out = c;
     return LDPC_OK;
+}
+
+// MacKay alist (P:4 "Any Binary Parity Check matrix ... can be
+// used"): "n m", "max_col_weight max_row_weight", the n column weights, the m
+// row weights, n lines of 1-based row indices per column, m lines of 1-based
+// column indices per row, each line zero-padded to the maximum weight.  Index
+// lists are written in ascending order.
+ldpc_status ldpc_code_write_alist(const ldpc_code *code, char *buf, size_t cap, size_t *len) {
+    if (!code || !len) return LDPC_ERR_ARG;
+    const int32_t n = code->n, m = code->m;
+    std::vector<int32_t> edge_row(size_t(std::max(code->nnz, 1)));
+    for (int32_t r = 0; r < m; ++r)
+        for (int32_t e = code->row_ptr[r]; e < code->row_ptr[r + 1]; ++e) edge_row[e] = r;
+    std::string s;
+    s.reserve(size_t(code->nnz) * 14 + size_t(n + m) * 4 + 64);
+    auto line = [&](const std::vector<int32_t> &v, int32_t pad_to) {
+        for (size_t i = 0; i < v.size(); ++i) {
+            if (i) s += ' ';
+            s += std::to_string(v[i]);
+        }
+        for (int32_t i = int32_t(v.size()); i < pad_to; ++i) {
+            if (i) s += ' ';
+            s += '0';
+        }
+        s += '\n';
+    };
+    line({n, m}, 0);
+    line({code->max_col_deg, code->max_row_deg}, 0);
+    std::vector<int32_t> v;
+    v.clear();
+    for (int32_t j = 0; j < n; ++j) v.push_back(code->var_ptr[j + 1] - code->var_ptr[j]);
+    line(v, 0);
+    v.clear();
+    for (int32_t r = 0; r < m; ++r) v.push_back(code->row_ptr[r + 1] - code->row_ptr[r]);
+    line(v, 0);
+    for (int32_t j = 0; j < n; ++j) {
+        v.clear();
+        for (int32_t t = code->var_ptr[j]; t < code->var_ptr[j + 1]; ++t) v.push_back(edge_row[code->var_edges[t]] + 1);
+        std::sort(v.begin(), v.end());
+        line(v, code->max_col_deg);
+    }
+    for (int32_t r = 0; r < m; ++r) {
+        v.assign(code->col_idx.begin() + code->row_ptr[r], code->col_idx.begin() + code->row_ptr[r + 1]);
+        for (auto &x : v) x += 1;
+        std::sort(v.begin(), v.end());
+        line(v, code->max_row_deg);
+    }
+    *len = s.size();
+    if (!buf) return LDPC_OK;
+    if (cap < s.size() + 1) return LDPC_ERR_DIM;
+    std::memcpy(buf, s.data(), s.size());
+    buf[s.size()] = '\0';
+    return LDPC_OK;
+}
+
+ldpc_status ldpc_code_from_alist(const char *text, size_t len, ldpc_code **out) {
+    if (!out) return LDPC_ERR_ARG;
+    *out = nullptr;
+    if (!text) return LDPC_ERR_ARG;
+    // split into lines of non-negative integers (blank lines skipped)
+    std::vector<std::vector<int64_t>> lines;
+    std::vector<int64_t> cur;
+    int64_t val = 0;
+    bool in_num = false;
+    for (size_t i = 0; i <= len; ++i) {
+        const char ch = i < len ? text[i] : '\n';
+        if (ch >= '0' && ch <= '9') {
+            val = val * 10 + (ch - '0');
+            if (val > (int64_t(1) << 31)) return LDPC_ERR_ARG;
+            in_num = true;
+            continue;
+        }
+        if (in_num) {
+            cur.push_back(val);
+            val = 0;
+            in_num = false;
+        }
+        if (ch == '\n') {
+            if (!cur.empty()) lines.push_back(cur);
+            cur.clear();
+        } else if (ch != ' ' && ch != '\t' && ch != '\r' && ch != '\0') {
+            return LDPC_ERR_ARG;
+        }
+    }
+    if (lines.size() < 4 || lines[0].size() != 2 || lines[1].size() != 2) return LDPC_ERR_ARG;
+    const int64_t n = lines[0][0], m = lines[0][1];
+    if (n <= 0 || m < 0 || n > (int64_t(1) << 28) || m > (int64_t(1) << 28)) return LDPC_ERR_ARG;
+    if (lines[2].size() != size_t(n) || lines[3].size() != size_t(m)) return LDPC_ERR_DIM;
+    if (lines.size() != size_t(4 + n + m)) return LDPC_ERR_DIM;
+    const int64_t maxc = lines[1][0], maxr = lines[1][1];
+    // rows -> CSR (1-based column indices, zeros are padding)
+    std::vector<int32_t> row_ptr(size_t(m) + 1, 0), col_idx;
+    for (int64_t r = 0; r < m; ++r) {
+        const auto &L = lines[size_t(4 + n + r)];
+        int64_t w = 0;
+        bool padding = false;
+        for (int64_t x : L) {
+            if (x == 0) { padding = true; continue; }
+            if (padding || x > n) return LDPC_ERR_DIM;          // index after padding, or out of range
+            col_idx.push_back(int32_t(x - 1));
+            ++w;
+        }
+        if (w != lines[3][size_t(r)] || w > maxr || int64_t(L.size()) > std::max<int64_t>(maxr, w)) return LDPC_ERR_DIM;
+        row_ptr[size_t(r) + 1] = int32_t(col_idx.size());
+    }
+    // columns must describe the same matrix
+    std::vector<std::vector<int32_t>> col_rows(static_cast<size_t>(n));
+    for (int64_t r = 0; r < m; ++r)
+        for (int32_t e = row_ptr[size_t(r)]; e < row_ptr[size_t(r) + 1]; ++e) col_rows[size_t(col_idx[e])].push_back(int32_t(r));
+    for (int64_t j = 0; j < n; ++j) {
+        const auto &L = lines[size_t(4 + j)];
+        std::vector<int32_t> rows;
+        bool padding = false;
+        for (int64_t x : L) {
+            if (x == 0) { padding = true; continue; }
+            if (padding || x > m) return LDPC_ERR_DIM;
+            rows.push_back(int32_t(x - 1));
+        }
+        if (int64_t(rows.size()) != lines[2][size_t(j)] || int64_t(rows.size()) > maxc ||
+            int64_t(L.size()) > std::max<int64_t>(maxc, int64_t(rows.size())))
+            return LDPC_ERR_DIM;
+        std::sort(rows.begin(), rows.end());
+        auto want = col_rows[size_t(j)];
+        std::sort(want.begin(), want.end());
+        if (rows != want) return LDPC_ERR_DIM;
+    }
+    return ldpc_code_from_csr(int32_t(m), int32_t(n), row_ptr.data(), col_idx.empty() ? nullptr : col_idx.data(), out);
 }
 
 // Standard-form generator, Eq. 2-3; reading Q13.
