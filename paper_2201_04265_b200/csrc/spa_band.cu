@@ -55,20 +55,26 @@ __device__ __forceinline__ bool cta_sync_or(bool p) { return __syncthreads_or(p 
 // wc > 3 (Table I codes, n = 1032) use small CTAs: the 256-thread bound leaves
 // room for the wider per-row state.
 // MODE 0: check-major E; 1: variable-major E (VM); 2: VM + 16-bit L offsets.
-template <int WR, int WC, int B0, bool ET, int MODE>
+// NFIX: 0, or the code length compiled in (the DVB-S2 short frame n = 16200 of
+// C4): sizes, region bases, band offsets and the row stride become immediates
+// (fewer integer instructions per edge-update; same arithmetic, same results).
+template <int WR, int WC, int B0, bool ET, int MODE, int NFIX = 0>
 __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const BandArgs a) {
     constexpr bool VM = MODE >= 1, L16 = MODE == 2;
     extern __shared__ __align__(16) char smem[];
     __shared__ long long s_frame;
     const DeviceCode &code = a.code;
-    const int n = code.n, mb = code.mb;
-    const int T = blockDim.x, tt = threadIdx.x, S = a.row_stride;
+    constexpr int TFIX = NFIX ? (((NFIX / WR + B0 - 1) / B0 + 31) / 32 * 32) : 0;
+    constexpr bool RFIX_SMEM = NFIX && size_t(WC + 1) * NFIX * 4 + 1024 <= 227 * 1024;
+    const int n = NFIX ? NFIX : code.n, mb = NFIX ? NFIX / WR : code.mb;
+    const int T = NFIX ? TFIX : int(blockDim.x), tt = threadIdx.x, S = NFIX ? TFIX : a.row_stride;
+    const bool r_in_smem = NFIX ? RFIX_SMEM : a.r_in_smem != 0;
     constexpr int NB = WC - 1;          // bands held in shared memory
     constexpr int B1 = NB * B0;         // max rows of bands >= 1 per thread
     const uint32_t lbase = uint32_t(NB) * uint32_t(n) * 4u;
     const uint32_t rbase = lbase + uint32_t(n) * 4u;
     float *Ls = reinterpret_cast<float *>(smem + lbase);
-    float *Rs = a.r_in_smem ? reinterpret_cast<float *>(smem + rbase) : a.r_global + size_t(blockIdx.x) * n;
+    float *Rs = r_in_smem ? reinterpret_cast<float *>(smem + rbase) : a.r_global + size_t(blockIdx.x) * n;
     const int32_t *lidx = code.band_lidx;
     const int32_t *vpos = code.band_vpos;
 
@@ -277,6 +283,14 @@ void *pick_b0_small(int b0, bool et, int vm) {
 
 // (wc, wr) instantiated: the BASELINE.json configs ((3, 4), (3, 6), (3, 12))
 // and the paper's Table I (wr = 12 with wc = 9, 6, 3).
+// Compile-time-n instantiations (NFIX): C4's n = 16200 with its auto mode.
+void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode) {
+    if (n == 16200 && wr == 6 && wc == 3 && b0 == 3 && mode == 2)
+        return et ? reinterpret_cast<void *>(&band_kernel<6, 3, 3, true, 2, 16200>)
+                  : reinterpret_cast<void *>(&band_kernel<6, 3, 3, false, 2, 16200>);
+    return nullptr;
+}
+
 void *pick_band_kernel(int wr, int wc, int b0, bool et, int vm) {
     if (wc == 3) {
         switch (wr) {
@@ -554,7 +568,8 @@ bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPla
     p.vm = variant == 4 || variant == 6 || (variant == 0 && (!p.r_in_smem || c.wc > 3));
     // 16-bit offsets (variant 6, auto with VM when n <= 16383): +2% on C4
     p.mode = p.vm ? (((variant == 6 || variant == 0) && c.n <= 16383) ? 2 : 1) : 0;
-    void *k = pick_band_kernel(c.wr, c.wc, b0, et, p.mode);
+    void *k = std::getenv("LDPC_NO_NFIX") ? nullptr : pick_band_kernel_fixed(c.n, c.wr, c.wc, b0, et, p.mode);
+    if (!k) k = pick_band_kernel(c.wr, c.wc, b0, et, p.mode);
     if (!k) return false;
     p.smem = p.r_in_smem ? with_r : base;
     p.threads = ((mb + b0 - 1) / b0 + 31) / 32 * 32;
