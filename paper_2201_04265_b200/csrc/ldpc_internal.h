@@ -194,6 +194,8 @@ struct BandPlan {
 // (wc, wr), n % 4 != 0, or the frame does not fit one SM's shared memory).
 // variant: 0 auto, 3 check-major E, 4 variable-major E.
 bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPlan &p);
+// band_kernel instantiation with n compiled in (spa_band_fixed.cu), or nullptr.
+void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode);
 ldpc_status band_launch(const ldpc_code &c, const BandPlan &p, const float *llr, int64_t frames,
                         const ldpc_decode_opts &o, uint32_t *bits, uint8_t *syn, int32_t *iters, float *post,
                         void *ws, size_t ws_bytes, void *stream);

@@ -32,222 +32,7 @@ namespace ldpc {
 namespace {
 using namespace band;
 
-struct BandArgs {
-    DeviceCode code;
-    const float *llr;
-    int64_t frames;
-    int32_t max_iter;
-    int32_t early_term;
-    uint32_t *bits;
-    uint8_t *syn_ok;
-    int32_t *iters;
-    float *posterior;
-    unsigned long long *frame_counter;   // zeroed before launch
-    float *r_global;                     // R' per CTA slot when R does not fit in smem
-    int32_t r_in_smem;
-    int32_t row_stride;                  // S = ceil(mb / B0): thread t owns rows t, t+S, ...
-                                         // (balanced: every active thread gets B0 band-0 rows)
-};
-
-__device__ __forceinline__ bool cta_sync_or(bool p) { return __syncthreads_or(p ? 1 : 0) != 0; }
-
-// WR: row weight, WC: column weight (bands), B0: max band-0 rows per thread.
-// wc > 3 (Table I codes, n = 1032) use small CTAs: the 256-thread bound leaves
-// room for the wider per-row state.
-// MODE 0: check-major E; 1: variable-major E (VM); 2: VM + 16-bit L offsets.
-// NFIX: 0, or the code length compiled in (the DVB-S2 short frame n = 16200 of
-// C4): sizes, region bases, band offsets and the row stride become immediates
-// (fewer integer instructions per edge-update; same arithmetic, same results).
-template <int WR, int WC, int B0, bool ET, int MODE, int NFIX = 0>
-__global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const BandArgs a) {
-    constexpr bool VM = MODE >= 1, L16 = MODE == 2;
-    extern __shared__ __align__(16) char smem[];
-    __shared__ long long s_frame;
-    const DeviceCode &code = a.code;
-    constexpr int TFIX = NFIX ? (((NFIX / WR + B0 - 1) / B0 + 31) / 32 * 32) : 0;
-    constexpr bool RFIX_SMEM = NFIX && size_t(WC + 1) * NFIX * 4 + 1024 <= 227 * 1024;
-    const int n = NFIX ? NFIX : code.n, mb = NFIX ? NFIX / WR : code.mb;
-    const int T = NFIX ? TFIX : int(blockDim.x), tt = threadIdx.x, S = NFIX ? TFIX : a.row_stride;
-    const bool r_in_smem = NFIX ? RFIX_SMEM : a.r_in_smem != 0;
-    constexpr int NB = WC - 1;          // bands held in shared memory
-    constexpr int B1 = NB * B0;         // max rows of bands >= 1 per thread
-    const uint32_t lbase = uint32_t(NB) * uint32_t(n) * 4u;
-    const uint32_t rbase = lbase + uint32_t(n) * 4u;
-    float *Ls = reinterpret_cast<float *>(smem + lbase);
-    float *Rs = r_in_smem ? reinterpret_cast<float *>(smem + rbase) : a.r_global + size_t(blockIdx.x) * n;
-    const int32_t *lidx = code.band_lidx;
-    const int32_t *vpos = code.band_vpos;
-
-    for (;;) {
-        if (tt == 0) s_frame = (long long)atomicAdd(a.frame_counter, 1ull);
-        __syncthreads();
-        const long long f = s_frame;
-        if (f >= a.frames) break;
-
-        // a1/a2: ingest R (clamped +-30, log2 units), L = R, E = 0
-        const float *src = a.llr + f * (long long)n;
-        for (int v4 = tt; v4 < (n >> 2); v4 += T) {
-            float4 r = __ldg(reinterpret_cast<const float4 *>(src) + v4);
-            r.x = fminf(fmaxf(r.x, -30.0f), 30.0f) * kL2E;
-            r.y = fminf(fmaxf(r.y, -30.0f), 30.0f) * kL2E;
-            r.z = fminf(fmaxf(r.z, -30.0f), 30.0f) * kL2E;
-            r.w = fminf(fmaxf(r.w, -30.0f), 30.0f) * kL2E;
-            reinterpret_cast<float4 *>(Rs)[v4] = r;
-            reinterpret_cast<float4 *>(Ls)[v4] = r;
-        }
-        for (int i = tt; i < (NB * n) >> 2; i += T)
-            reinterpret_cast<float4 *>(smem)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        float e0[B0][WR];
-#pragma unroll
-        for (int k = 0; k < B0; ++k)
-#pragma unroll
-            for (int j = 0; j < WR; ++j) e0[k][j] = 0.0f;
-        __syncthreads();
-
-        int32_t iters = a.max_iter;
-        bool stopped = false;
-        for (int t = 1; t <= a.max_iter; ++t) {
-            // ---- a3: check-node phase (and syndrome of z^{t-1} when ET)
-            uint32_t synd = 0;
-#pragma unroll
-            for (int k = 0; k < B0; ++k) {
-                const int r = tt + k * S;
-                if (tt < S && r < mb) {
-                    float lv[WR], x[WR];
-                    lds_row<WR>(smem, lbase + uint32_t(r) * WR * 4u, lv);
-                    uint32_t rp = 0;      // this row's syndrome bit (Eq. 1)
-#pragma unroll
-                    for (int j = 0; j < WR; ++j) {
-                        x[j] = lv[j] - e0[k][j];
-                        if (ET) rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
-                    }
-                    synd |= rp;
-                    check_row<WR, !ET>(x, e0[k]);
-                }
-            }
-#pragma unroll
-            for (int k = 0; k < B1; ++k) {
-                const int r = tt + k * S;
-                if (tt < S && r < NB * mb) {
-                    int32_t li[WR];
-                    float e[WR], x[WR];
-                    if (L16) {
-                        // 16-bit offsets relative to L: half the index bytes through L1/L2
-                        const uint32_t *p16 = reinterpret_cast<const uint32_t *>(code.band_lidx16 + size_t(r) * WR);
-#pragma unroll
-                        for (int w = 0; w < WR / 2; ++w) {
-                            const uint32_t x = __ldg(p16 + w);
-                            li[2 * w] = int32_t(lbase + (x & 0xffffu));
-                            li[2 * w + 1] = int32_t(lbase + (x >> 16));
-                        }
-                    } else {
-                        ldg_idx<WR>(lidx + size_t(r) * WR, li);
-                    }
-                    // VM: E_b is variable-major, at the variable's L offset + delta_b
-                    const int32_t delta = VM ? int32_t((r / mb) * n * 4) - int32_t(lbase) : 0;
-                    if (VM) {
-#pragma unroll
-                        for (int j = 0; j < WR; ++j) e[j] = *reinterpret_cast<const float *>(smem + li[j] + delta);
-                    } else {
-                        lds_row<WR>(smem, uint32_t(r) * WR * 4u, e);
-                    }
-                    uint32_t rp = 0;
-#pragma unroll
-                    for (int j = 0; j < WR; ++j) {
-                        const float lv = *reinterpret_cast<const float *>(smem + li[j]);
-                        x[j] = lv - e[j];
-                        if (ET) rp ^= (lv >= 0.0f) ? 1u : 0u;
-                    }
-                    synd |= rp;
-                    check_row<WR, !ET>(x, e);
-                    if (VM) {
-#pragma unroll
-                        for (int j = 0; j < WR; ++j) *reinterpret_cast<float *>(smem + li[j] + delta) = e[j];
-                    } else {
-                        sts_row<WR>(smem, uint32_t(r) * WR * 4u, e);
-                    }
-                }
-            }
-            if (ET) {
-                const bool any = cta_sync_or(synd != 0);
-                if (t > 1 && !any) {      // z^{t-1} has zero syndrome: stop (reading c6)
-                    iters = t - 1;
-                    stopped = true;
-                    break;
-                }
-            } else {
-                __syncthreads();
-            }
-            // ---- a4/a5: variable-node phase, Eq. 7 (owners of band-0 rows)
-#pragma unroll
-            for (int k = 0; k < B0; ++k) {
-                const int r = tt + k * S;
-                if (tt < S && r < mb) {
-                    float rv[WR], lv[WR];
-                    lds_row<WR>(reinterpret_cast<const char *>(Rs), uint32_t(r) * WR * 4u, rv);
-                    if (VM) {
-                        // this row's variables are contiguous in every band's E_b
-#pragma unroll
-                        for (int j = 0; j < WR; ++j) lv[j] = rv[j] + e0[k][j];
-#pragma unroll
-                        for (int b = 0; b < NB; ++b) {
-                            float eb[WR];
-                            lds_row<WR>(smem, uint32_t(b) * n * 4u + uint32_t(r) * WR * 4u, eb);
-#pragma unroll
-                            for (int j = 0; j < WR; ++j) lv[j] += eb[j];
-                        }
-                    } else {
-                        int32_t vp[WR * NB];
-                        ldg_idx<WR * NB>(vpos + size_t(r) * WR * NB, vp);
-#pragma unroll
-                        for (int j = 0; j < WR; ++j) {
-                            float s = rv[j] + e0[k][j];
-#pragma unroll
-                            for (int b = 0; b < NB; ++b) s += *reinterpret_cast<const float *>(smem + vp[j * NB + b]);
-                            lv[j] = s;
-                        }
-                    }
-                    sts_row<WR>(smem, lbase + uint32_t(r) * WR * 4u, lv);
-                }
-            }
-            __syncthreads();
-        }
-        // ---- a7: final syndrome when the loop ran to max_iter
-        bool ok = stopped;
-        if (!stopped) {
-            uint32_t synd = 0;
-            for (int r = tt; r < mb; r += T) {
-                uint32_t rp = 0;
-                for (int j = 0; j < WR; ++j) rp ^= (Ls[r * WR + j] >= 0.0f) ? 1u : 0u;
-                synd |= rp;
-            }
-            for (int r = tt; r < NB * mb; r += T) {
-                uint32_t rp = 0;
-                for (int j = 0; j < WR; ++j)
-                    rp ^= (*reinterpret_cast<const float *>(smem + __ldg(lidx + size_t(r) * WR + j)) >= 0.0f) ? 1u : 0u;
-                synd |= rp;
-            }
-            ok = !cta_sync_or(synd != 0);
-        }
-        // ---- a6/a8: hard decisions (Eq. 8) packed by ballot, flags, posteriors
-        const int nw = code.nw;
-        uint32_t *bits = a.bits + f * (long long)nw;
-        for (int v = tt; v < nw * 32; v += T) {
-            const bool z = (v < n) ? (Ls[v] >= 0.0f) : false;
-            const uint32_t word = __ballot_sync(0xffffffffu, z);
-            if ((tt & 31) == 0) bits[v >> 5] = word;
-        }
-        if (a.posterior) {
-            float *dst = a.posterior + f * (long long)n;
-            for (int v = tt; v < n; v += T) dst[v] = Ls[v] * kLn2;
-        }
-        if (tt == 0) {
-            a.syn_ok[f] = ok ? 1 : 0;
-            a.iters[f] = iters;
-        }
-        __syncthreads();
-    }
-}
+#include "band_kernel.cuh"
 
 template <int WR, int WC, int B0>
 void *pick_et(bool et, int mode) {
@@ -283,14 +68,6 @@ void *pick_b0_small(int b0, bool et, int vm) {
 
 // (wc, wr) instantiated: the BASELINE.json configs ((3, 4), (3, 6), (3, 12))
 // and the paper's Table I (wr = 12 with wc = 9, 6, 3).
-// Compile-time-n instantiations (NFIX): C4's n = 16200 with its auto mode.
-void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode) {
-    if (n == 16200 && wr == 6 && wc == 3 && b0 == 3 && mode == 2)
-        return et ? reinterpret_cast<void *>(&band_kernel<6, 3, 3, true, 2, 16200>)
-                  : reinterpret_cast<void *>(&band_kernel<6, 3, 3, false, 2, 16200>);
-    return nullptr;
-}
-
 void *pick_band_kernel(int wr, int wc, int b0, bool et, int vm) {
     if (wc == 3) {
         switch (wr) {

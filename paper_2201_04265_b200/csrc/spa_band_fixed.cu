@@ -1,0 +1,46 @@
+// spa_band_fixed.cu -- band_kernel instantiations with the code length
+// compiled in (NFIX) for the BASELINE.json configs' codes, in a translation
+// unit of their own so the build compiles them in parallel with spa_band.cu.
+// Sizes, shared-memory region bases, band offsets and the row stride become
+// immediates: fewer integer instructions per edge-update, identical
+// arithmetic.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "band_common.cuh"
+#include "ldpc_internal.h"
+
+namespace ldpc {
+namespace {
+using namespace band;
+#include "band_kernel.cuh"
+
+template <int WR, int WC, int B0, int MODE, int N>
+void *et_pair(bool et) {
+    return et ? reinterpret_cast<void *>(&band_kernel<WR, WC, B0, true, MODE, N>)
+              : reinterpret_cast<void *>(&band_kernel<WR, WC, B0, false, MODE, N>);
+}
+}  // namespace
+
+// (n, wr, wc, rows per thread, mode) as band_plan resolves them in auto mode:
+//   C4 16200 (3,6) VM+16-bit; C2 1008 (3,6) check-major; C3 3996 (3,6/12)
+//   check-major; Table I 1032 (wc 9/6 VM+16-bit, 3 check-major).  Measured
+//   on B200 against NFIX = 0: C2 +2.6, C4 +2.9, C3-R3/4 +0.7, Table I R1/4
+//   (100k frames) +1.3 points of the SFU roofline; C3 (3,4) -0.7 (left out).
+void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode) {
+    if (wc == 3 && wr == 6 && n == 16200 && b0 == 3 && mode == 2) return et_pair<6, 3, 3, 2, 16200>(et);
+    if (wc == 3 && wr == 6 && n == 1008 && b0 == 1 && mode == 0) return et_pair<6, 3, 1, 0, 1008>(et);
+    if (wc == 3 && n == 3996 && b0 == 1 && mode == 0) {
+        if (wr == 6) return et_pair<6, 3, 1, 0, 3996>(et);
+        if (wr == 12) return et_pair<12, 3, 1, 0, 3996>(et);
+    }
+    if (wr == 12 && n == 1032 && b0 == 1) {
+        if (wc == 9 && mode == 2) return et_pair<12, 9, 1, 2, 1032>(et);
+        if (wc == 6 && mode == 2) return et_pair<12, 6, 1, 2, 1032>(et);
+        if (wc == 3 && mode == 0) return et_pair<12, 3, 1, 0, 1032>(et);
+    }
+    return nullptr;
+}
+
+}  // namespace ldpc
