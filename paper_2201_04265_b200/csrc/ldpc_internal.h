@@ -88,11 +88,11 @@ inline int band_cluster_size(int32_t n, int32_t wc, int32_t wr) {
 // mbq = n / wr / C rows of every band and the nq = mbq wr variables of its
 // band-0 rows.  Compute threads and rows per thread (= V-phase chunks H) of a
 // CTA (the launch adds one producer warp):
-inline int xband_rows_per_thread(int32_t mbq) {
+constexpr int xband_rows_per_thread(int32_t mbq) {
     const int b0 = mbq > 0 ? (mbq + 1023) / 1024 : 1;
     return b0 == 3 ? 4 : b0;                      // instantiated: 1, 2, 4
 }
-inline int xband_threads(int32_t mbq) {
+constexpr int xband_threads(int32_t mbq) {
     const int b0 = xband_rows_per_thread(mbq);
     return ((mbq + b0 - 1) / b0 + 31) / 32 * 32;
 }

@@ -149,13 +149,15 @@ __device__ __forceinline__ void mbar_arrive_local(uint32_t bar) {
 // as soon as every compute warp arrived on its chunk barrier -- no CTA-wide
 // barrier inside the iteration loop.
 // MAXT: launch bound (768 lets a 736-thread C5 block keep 85 registers).
-template <int WR, int WC, int H, int C, int MAXT>
+// NFIX: 0, or the code length compiled in (C5's n = 64800, the DVB-S2 normal
+// frame): sizes and loop bounds become immediates.
+template <int WR, int WC, int H, int C, int MAXT, int NFIX = 0>
 __global__ void __launch_bounds__(MAXT, 1) xband_kernel(const XArgs a) {
     extern __shared__ __align__(128) char smem[];
     constexpr int NB = WC - 1;
     const DeviceCode &code = a.code;
-    const int n = code.n, mb = code.mb, mbq = mb / C, nq = n / C;
-    const int TW = blockDim.x - 32, tt = threadIdx.x, lane = tt & 31;
+    const int n = NFIX ? NFIX : code.n, mb = NFIX ? NFIX / WR : code.mb, mbq = mb / C, nq = n / C;
+    const int TW = NFIX ? xband_threads(NFIX / WR / C) : int(blockDim.x) - 32, tt = threadIdx.x, lane = tt & 31;
     const bool producer = tt >= TW;
     const uint32_t cap_b = uint32_t(code.xcap) * 4u;
     const uint32_t q = cluster_ctarank();
@@ -445,7 +447,11 @@ bool xcluster_plan(const ldpc_code &c, int64_t frames, bool et, XClusterPlan &p)
     const int mbq = c.n / c.wr / C;
     const int H = xband_rows_per_thread(mbq);
     p.threads = xband_threads(mbq) + 32;          // compute warps + the producer warp
-    void *k = pick_xband_kernel(c.wr, c.wc, H, C, p.threads);
+    void *k = nullptr;
+    // compile-time n for C5 (n = 64800, C = 8, 736 threads)
+    if (c.n == 64800 && c.wr == 6 && c.wc == 3 && C == 8 && H == 2 && p.threads <= 768 && !std::getenv("LDPC_NO_NFIX"))
+        k = reinterpret_cast<void *>(&xband_kernel<6, 3, 2, 8, 768, 64800>);
+    if (!k) k = pick_xband_kernel(c.wr, c.wc, H, C, p.threads);
     if (!k) return false;
     p.kernel = k;
     p.cluster = C;
