@@ -55,8 +55,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--eager", action="store_true", help="launch the step's kernels eagerly instead of replaying a CUDA graph")
-    ap.add_argument("--mode", choices=["batch", "stream"], default="batch",
-                    help="stream = frames decoded one per ldpc_decode call, serially (the paper's stream mode)")
+    ap.add_argument("--mode", choices=["batch", "stream", "simulate"], default="batch",
+                    help="stream = frames decoded one per ldpc_decode call, serially (the paper's stream mode); "
+                         "simulate = BER-simulation pipeline, fused (ldpc_decode_simulate) vs unfused")
     return ap.parse_args()
 
 
@@ -116,6 +117,77 @@ def run_stream(args):
                       "edge_updates_per_s": wl.edges * iters / (ms * 1e-3), "mean_iterations": iters,
                       "config": workload_config(wl, 1, 1), "frames_timed": args.steps * G,
                       "note": "one CTA decodes the frame; serial calls replayed from a CUDA graph"}), flush=True)
+    return 0
+
+
+def run_simulate(args):
+    """BER-simulation pipeline on fresh frames every step:
+    gen_info -> encode -> [channel -> decode -> count] (unfused, 4 n bytes of
+    LLRs per frame through HBM) vs gen_info -> encode -> ldpc_decode_simulate
+    (fused: channel draw in the decode prologue, counters in its epilogue).
+    Both arms decode the same frames; their counters must agree."""
+    import torch
+
+    import paper_2201_04265_b200 as L
+    torch.cuda.set_device(0)
+    wl = W.ALL[args.config]
+    F = args.frames or min(wl.frames, 32768)
+    code = L.ldpc_code_bind_device(L.ldpc_make_G(L.ldpc_make_H(wl.n, wl.wc, wl.wr, W.CODE_SEED)))
+    k, n = code.info.k, code.info.n
+    info = torch.empty((F, L.words(k)), dtype=torch.int32, device="cuda")
+    cw = torch.empty((F, L.words(n)), dtype=torch.int32, device="cuda")
+    llr = torch.empty((F, n), dtype=torch.float32, device="cuda")
+    bits = torch.empty((F, L.words(n)), dtype=torch.int32, device="cuda")
+    syn = torch.empty(F, dtype=torch.uint8, device="cuda")
+    its = torch.empty(F, dtype=torch.int32, device="cuda")
+    ctr_u = torch.zeros(6, dtype=torch.int64, device="cuda")
+    ctr_f = torch.zeros(6, dtype=torch.int64, device="cuda")
+    tmp = torch.zeros(6, dtype=torch.int64, device="cuda")
+    wsb = max(L.ldpc_decode_workspace_bytes(code, F, wl.max_iter, wl.early_term, 6 if wl.n == 16200 else 0), 256)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    seed, sigma = wl.frame_seeds[0], wl.sigma()
+    band = 6 if wl.n == 16200 else 0      # both arms on the band kernel (the fused path's decoder)
+
+    def unfused(frame0):
+        L.ldpc_gen_info(seed, frame0, F, k, info)
+        L.ldpc_encode(code, info, cw, F)
+        L.ldpc_channel(code, seed, frame0, F, cw, sigma, llr)
+        L.ldpc_decode(code, llr, F, bits, syn, its, None, ws, wl.max_iter, wl.early_term, band)
+        tmp.zero_()
+        L.ldpc_count_errors(code, info, bits, cw, syn, its, F, tmp)
+        ctr_u.add_(tmp)
+
+    def fused(frame0):
+        L.ldpc_gen_info(seed, frame0, F, k, info)
+        L.ldpc_encode(code, info, cw, F)
+        L.ldpc_decode_simulate(code, seed, frame0, F, sigma, info, cw, bits, syn, its, ctr_f, ws,
+                               wl.max_iter, wl.early_term, band)
+
+    res = {}
+    for name, fn in (("unfused", unfused), ("fused", fused)):
+        for w in range(args.warmup):
+            fn(10**9 + w * F)
+        torch.cuda.synchronize()
+        (ctr_u if name == "unfused" else ctr_f).zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(0) as clk:
+            e0.record()
+            for st in range(args.steps):
+                fn(st * F)
+            e1.record()
+            torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        res[name] = {"ms_per_step": ms, "info_gbit_s": F * k / (ms * 1e-3) / 1e9, "clocks": clk.summary()}
+    cu, cf = ctr_u.tolist(), ctr_f.tolist()
+    assert cu == cf, (cu, cf)
+    print(json.dumps({"mode": "simulate", "metric": "BER-simulation throughput (info Gbit/s)",
+                      "value": res["fused"]["info_gbit_s"], "unit": "Gbit/s",
+                      "unfused_value": res["unfused"]["info_gbit_s"], "fused": res["fused"], "unfused": res["unfused"],
+                      "llr_bytes_saved_per_step": 2 * F * n * 4, "counters": cf,
+                      "ber_info": cf[0] / max(cf[5] * k, 1), "fer": cf[2] / max(cf[5], 1),
+                      "config": workload_config(wl, F, 1), "steps": args.steps, "warmup": args.warmup,
+                      "note": "each step: gen_info + encode + (channel + decode + count | fused simulate) on new frames; "
+                              "counters of the two arms identical"}), flush=True)
     return 0
 
 
@@ -266,6 +338,8 @@ def main():
         return run_reference(args)
     if args.mode == "stream":
         return run_stream(args)
+    if args.mode == "simulate":
+        return run_simulate(args)
 
     import numpy as np
     import torch

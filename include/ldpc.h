@@ -185,6 +185,24 @@ ldpc_status ldpc_decode(const ldpc_code *code, const float *d_llr, int64_t frame
                         uint8_t *d_syndrome_ok, int32_t *d_iters, float *d_posterior,
                         void *d_ws, size_t ws_bytes, void *stream);
 
+/* Fused simulate step (Eq. 4-8): for
+ * frames frame0 .. frame0+frames-1 the decoder draws the channel LLRs in its
+ * prologue exactly as ldpc_channel(code, seed, frame0, frames, d_cw, sigma)
+ * would (same counters, same roundings), decodes them as ldpc_decode with
+ * `opts`, and ADDS the frames' counters (as ldpc_count_errors) to
+ * d_counters6 -- no frames*n*4-byte LLR buffer, one kernel launch.
+ *   d_info: frames*ceil(k/32) uint32 info bits; d_cw: their codewords
+ *   (ldpc_encode); d_bits / d_syndrome_ok / d_iters as ldpc_decode; no
+ *   posterior.  Workspace: ldpc_decode_workspace_bytes for the same code,
+ *   frames and opts.  Gallager (3,6) codes whose frame fits one SM, opts
+ *   variant 0/3/4/6 (else LDPC_ERR_UNSUPPORTED); needs make_G before
+ *   bind_device (LDPC_ERR_STATE); sigma > 0. */
+ldpc_status ldpc_decode_simulate(const ldpc_code *code, uint64_t seed, int64_t frame0, int64_t frames,
+                                 double sigma, const uint32_t *d_info, const uint32_t *d_cw,
+                                 const ldpc_decode_opts *opts, uint32_t *d_bits, uint8_t *d_syndrome_ok,
+                                 int32_t *d_iters, int64_t *d_counters6, void *d_ws, size_t ws_bytes,
+                                 void *stream);
+
 /* ---------------------------------------------------------------- harness helpers */
 
 /* Info bits (reading c4): word w of frame f = lane w%4 of Philox4x32-10 with

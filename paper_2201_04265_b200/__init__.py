@@ -194,6 +194,17 @@ def ldpc_decode(code: Code, d_llr, frames: int, d_bits, d_syndrome_ok, d_iters, 
          _stream(stream))
 
 
+def ldpc_decode_simulate(code: Code, seed: int, frame0: int, frames: int, sigma: float, d_info, d_cw,
+                         d_bits, d_syndrome_ok, d_iters, d_counters6, d_ws=None, max_iter: int = 50,
+                         early_term: bool = False, variant: int = 0, stream=None) -> None:
+    """Fused channel -> decode -> count (ldpc.h); counters are ADDED to d_counters6."""
+    o = _opts(max_iter, early_term, variant)
+    ws_bytes = 0 if d_ws is None else d_ws.numel() * d_ws.element_size()
+    call("ldpc_decode_simulate", code.handle, C.c_uint64(int(seed)), int(frame0), int(frames), float(sigma),
+         _ptr(d_info), _ptr(d_cw), C.byref(o), _ptr(d_bits), _ptr(d_syndrome_ok), _ptr(d_iters),
+         _ptr(d_counters6), _ptr(d_ws), C.c_size_t(ws_bytes), _stream(stream))
+
+
 def ldpc_gen_info(seed: int, frame0: int, frames: int, k: int, d_info, stream=None) -> None:
     call("ldpc_gen_info", C.c_uint64(int(seed)), int(frame0), int(frames), int(k), _ptr(d_info),
          _stream(stream))

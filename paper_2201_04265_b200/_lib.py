@@ -18,7 +18,7 @@ EXPORTED = [
     "ldpc_make_H", "ldpc_code_from_csr", "ldpc_code_from_alist", "ldpc_code_write_alist", "ldpc_make_G", "ldpc_code_query", "ldpc_code_copy_H",
     "ldpc_code_copy_csr", "ldpc_code_copy_perm", "ldpc_code_copy_P", "ldpc_code_bind_device",
     "ldpc_code_free", "ldpc_status_str", "ldpc_encode", "ldpc_decode_workspace_bytes", "ldpc_decode",
-    "ldpc_decode_variant",
+    "ldpc_decode_variant", "ldpc_decode_simulate",
     "ldpc_gen_info", "ldpc_channel", "ldpc_count_errors", "ldpc_partition", "ldpc_debug_phi",
 ]
 
@@ -67,6 +67,7 @@ def lib() -> C.CDLL:
             "ldpc_decode_workspace_bytes": [vp, i64, vp, vp],
             "ldpc_decode_variant": [vp, i64, vp, vp],
             "ldpc_decode": [vp, vp, i64, vp, vp, vp, vp, vp, vp, sz, vp],
+            "ldpc_decode_simulate": [vp, u64, i64, i64, C.c_double, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp],
             "ldpc_gen_info": [u64, i64, i64, i32, vp, vp],
             "ldpc_channel": [vp, u64, i64, i64, vp, C.c_double, vp, vp],
             "ldpc_count_errors": [vp, vp, vp, vp, vp, vp, i64, vp, vp],

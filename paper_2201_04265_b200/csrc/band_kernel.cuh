@@ -20,6 +20,14 @@ struct BandArgs {
     int32_t r_in_smem;
     int32_t row_stride;                  // S = ceil(mb / B0): thread t owns rows t, t+S, ...
                                          // (balanced: every active thread gets B0 band-0 rows)
+    // GEN (fused simulate, N4): R drawn in the prologue from (seed, frame0 + f)
+    // and the codeword, counters added in the epilogue
+    uint64_t seed;
+    int64_t frame0;
+    double sigma;
+    const uint32_t *cw;
+    const uint32_t *info;
+    unsigned long long *counters;        // int64[6], as ldpc_count_errors
 };
 
 __device__ __forceinline__ bool cta_sync_or(bool p) { return __syncthreads_or(p ? 1 : 0) != 0; }
@@ -31,7 +39,11 @@ __device__ __forceinline__ bool cta_sync_or(bool p) { return __syncthreads_or(p 
 // NFIX: 0, or the code length compiled in (the DVB-S2 short frame n = 16200 of
 // C4): sizes, region bases, band offsets and the row stride become immediates
 // (fewer integer instructions per edge-update; same arithmetic, same results).
-template <int WR, int WC, int B0, bool ET, int MODE, int NFIX = 0>
+// GEN: fused simulate (ldpc_decode_simulate): the prologue draws R
+// exactly as ldpc_channel does (channel_common.cuh) instead of loading it, and
+// the epilogue accumulates the counters of ldpc_count_errors per CTA (flushed
+// with six atomics when the CTA runs out of frames).
+template <int WR, int WC, int B0, bool ET, int MODE, int NFIX = 0, bool GEN = false>
 __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const BandArgs a) {
     constexpr bool VM = MODE >= 1, L16 = MODE == 2;
     extern __shared__ __align__(16) char smem[];
@@ -51,22 +63,43 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
     const int32_t *lidx = code.band_lidx;
     const int32_t *vpos = code.band_vpos;
 
+    unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};       // GEN: this CTA's counters (thread 0)
+    __shared__ int s_err[2];
     for (;;) {
         if (tt == 0) s_frame = (long long)atomicAdd(a.frame_counter, 1ull);
+        if (GEN && tt < 2) s_err[tt] = 0;
         __syncthreads();
         const long long f = s_frame;
         if (f >= a.frames) break;
 
         // a1/a2: ingest R (clamped +-30, log2 units), L = R, E = 0
-        const float *src = a.llr + f * (long long)n;
-        for (int v4 = tt; v4 < (n >> 2); v4 += T) {
-            float4 r = __ldg(reinterpret_cast<const float4 *>(src) + v4);
-            r.x = fminf(fmaxf(r.x, -30.0f), 30.0f) * kL2E;
-            r.y = fminf(fmaxf(r.y, -30.0f), 30.0f) * kL2E;
-            r.z = fminf(fmaxf(r.z, -30.0f), 30.0f) * kL2E;
-            r.w = fminf(fmaxf(r.w, -30.0f), 30.0f) * kL2E;
-            reinterpret_cast<float4 *>(Rs)[v4] = r;
-            reinterpret_cast<float4 *>(Ls)[v4] = r;
+        if constexpr (GEN) {
+            // R of frame frame0 + f as ldpc_channel draws it (Eq. 4)
+            const uint32_t *c = a.cw + f * (long long)code.nw;
+            const uint64_t fr = uint64_t(a.frame0 + f);
+            for (int v4 = tt; v4 < (n >> 2); v4 += T) {
+                double z[4];
+                channel_normals(a.seed, fr, v4, z);
+                const uint32_t word = __ldg(c + (v4 >> 3)) >> ((4 * v4) & 31);
+                float4 r;
+                r.x = fminf(fmaxf(channel_llr(word & 1u, a.sigma, z[0]), -30.0f), 30.0f) * kL2E;
+                r.y = fminf(fmaxf(channel_llr(word & 2u, a.sigma, z[1]), -30.0f), 30.0f) * kL2E;
+                r.z = fminf(fmaxf(channel_llr(word & 4u, a.sigma, z[2]), -30.0f), 30.0f) * kL2E;
+                r.w = fminf(fmaxf(channel_llr(word & 8u, a.sigma, z[3]), -30.0f), 30.0f) * kL2E;
+                reinterpret_cast<float4 *>(Rs)[v4] = r;
+                reinterpret_cast<float4 *>(Ls)[v4] = r;
+            }
+        } else {
+            const float *src = a.llr + f * (long long)n;
+            for (int v4 = tt; v4 < (n >> 2); v4 += T) {
+                float4 r = __ldg(reinterpret_cast<const float4 *>(src) + v4);
+                r.x = fminf(fmaxf(r.x, -30.0f), 30.0f) * kL2E;
+                r.y = fminf(fmaxf(r.y, -30.0f), 30.0f) * kL2E;
+                r.z = fminf(fmaxf(r.z, -30.0f), 30.0f) * kL2E;
+                r.w = fminf(fmaxf(r.w, -30.0f), 30.0f) * kL2E;
+                reinterpret_cast<float4 *>(Rs)[v4] = r;
+                reinterpret_cast<float4 *>(Ls)[v4] = r;
+            }
         }
         for (int i = tt; i < (NB * n) >> 2; i += T)
             reinterpret_cast<float4 *>(smem)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -218,7 +251,37 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
             a.syn_ok[f] = ok ? 1 : 0;
             a.iters[f] = iters;
         }
+        if constexpr (GEN) {
+            // a9 counters of this frame (reading Q14): info-bit errors
+            // at perm[0..k), codeword-bit errors, frame error, undetected error
+            const uint32_t *c = a.cw + f * (long long)code.nw;
+            const uint32_t *m = a.info + f * (long long)code.kw;
+            int ie = 0, ce = 0;
+            for (int t = tt; t < code.k; t += T) {
+                const int v = __ldg(code.perm + t);
+                ie += (Ls[v] >= 0.0f) != bool((__ldg(m + (t >> 5)) >> (t & 31)) & 1u);
+            }
+            for (int v = tt; v < n; v += T) ce += (Ls[v] >= 0.0f) != bool((__ldg(c + (v >> 5)) >> (v & 31)) & 1u);
+            ie = __reduce_add_sync(0xffffffffu, ie);
+            ce = __reduce_add_sync(0xffffffffu, ce);
+            if ((tt & 31) == 0) {
+                atomicAdd(&s_err[0], ie);
+                atomicAdd(&s_err[1], ce);
+            }
+            __syncthreads();
+            if (tt == 0) {
+                cnt[0] += unsigned(s_err[0]);
+                cnt[1] += unsigned(s_err[1]);
+                cnt[2] += s_err[0] > 0;
+                cnt[3] += (ok && s_err[1] > 0);
+                cnt[4] += unsigned(iters);
+                cnt[5] += 1;
+            }
+        }
         __syncthreads();
     }
+    if (GEN && tt == 0)
+        for (int i = 0; i < 6; ++i)
+            if (cnt[i]) atomicAdd(a.counters + i, cnt[i]);
 }
 

@@ -6,28 +6,11 @@
 #include <algorithm>
 #include <cstdint>
 
+#include "channel_common.cuh"
 #include "ldpc_internal.h"
 
 namespace ldpc {
 namespace {
-
-// ---------------------------------------------------------------------------
-// Philox4x32-10 (Salmon et al., SC'11): the counter-based generator the
-// workload recipe fixes.
-struct U4 {
-    uint32_t x, y, z, w;
-};
-__device__ __forceinline__ U4 philox(U4 c, uint32_t k0, uint32_t k1) {
-#pragma unroll
-    for (int r = 0; r < 10; ++r) {
-        const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
-        const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
-        c = U4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
-        k0 += 0x9E3779B9u;
-        k1 += 0xBB67AE85u;
-    }
-    return c;
-}
 
 // ---------------------------------------------------------------------------
 // Encoder, Eq. 3 with G in standard form: the parity bits
@@ -166,40 +149,20 @@ __global__ void channel_kernel(uint64_t seed, int64_t frame0, int64_t frames, in
     const int nw = (n + 31) / 32;
     const int groups = (n + 3) / 4;
     const int64_t total = frames * groups;
-    const double two_pi = 6.283185307179586476925286766559;
-    const double inv32 = 1.0 / 4294967296.0;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t f = i / groups;
         const int j = int(i - f * groups);
         const uint64_t fr = uint64_t(frame0 + f);
-        U4 r = philox(U4{uint32_t(j), uint32_t(fr), uint32_t(fr >> 32), 1u}, uint32_t(seed), uint32_t(seed >> 32));
         double z[4];
-        {
-            const double rad = sqrt(-2.0 * log((double(r.x) + 1.0) * inv32));
-            double sn, cs;
-            sincos(two_pi * (double(r.y) * inv32), &sn, &cs);
-            z[0] = rad * cs;
-            z[1] = rad * sn;
-        }
-        {
-            const double rad = sqrt(-2.0 * log((double(r.z) + 1.0) * inv32));
-            double sn, cs;
-            sincos(two_pi * (double(r.w) * inv32), &sn, &cs);
-            z[2] = rad * cs;
-            z[3] = rad * sn;
-        }
+        channel_normals(seed, fr, j, z);
         const uint32_t *c = cw + f * nw;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int v = 4 * j + q;
             if (v < n) {
-                const double x = ((__ldg(c + (v >> 5)) >> (v & 31)) & 1u) ? 1.0 : -1.0;
-                // y = x + sigma z, R = 2y / sigma^2, with no FMA contraction so the
-                // fp64 roundings are those of the plain formula
-                const double y = __dadd_rn(x, __dmul_rn(sigma, z[q]));
-                double l = __ddiv_rn(__dmul_rn(2.0, y), __dmul_rn(sigma, sigma));
-                l = fmin(fmax(l, -30.0), 30.0);
-                llr[f * n + v] = float(l);
+                const bool one = (__ldg(c + (v >> 5)) >> (v & 31)) & 1u;
+                const float l = channel_llr(one, sigma, z[q]);
+                llr[f * n + v] = l;
             }
         }
     }

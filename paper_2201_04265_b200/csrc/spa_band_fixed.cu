@@ -14,6 +14,7 @@
 namespace ldpc {
 namespace {
 using namespace band;
+#include "channel_common.cuh"
 #include "band_kernel.cuh"
 
 template <int WR, int WC, int B0, int MODE, int N>
