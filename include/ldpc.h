@@ -90,6 +90,16 @@ ldpc_status ldpc_make_H(int32_t n, int32_t wc, int32_t wr, uint64_t seed, ldpc_c
 ldpc_status ldpc_code_from_csr(int32_t m, int32_t n, const int32_t *row_ptr,
                                const int32_t *col_idx, ldpc_code **out);
 
+/* make_G on the GPU: the same elimination and result as
+ * ldpc_make_G (rank, k, perm, P bit-identical: the reduced row echelon form is
+ * unique), run as one cooperative kernel over H bit-packed in the caller's
+ * device workspace (d_ws, >= ldpc_make_G_device_workspace_bytes, 256-byte
+ * aligned; C5: ~1 GB).  Synchronises `stream`; the code's host image is
+ * updated as by ldpc_make_G (bind_device again afterwards).  Errors as
+ * ldpc_make_G, LDPC_ERR_CUDA on a device failure. */
+ldpc_status ldpc_make_G_device_workspace_bytes(const ldpc_code *code, size_t *bytes);
+ldpc_status ldpc_make_G_device(ldpc_code *code, void *d_ws, size_t ws_bytes, void *stream);
+
 /* MacKay alist text (P:4): "n m", "max_col_weight
  * max_row_weight", the n column weights, the m row weights, n lines of 1-based
  * row indices per column and m lines of 1-based column indices per row, each

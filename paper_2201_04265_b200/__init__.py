@@ -111,6 +111,17 @@ def ldpc_make_G(code: Code) -> Code:
     return code
 
 
+def ldpc_make_G_device(code: Code, device=None, stream=None) -> Code:
+    """make_G on the GPU (same result as ldpc_make_G); workspace from torch."""
+    import torch
+    n = C.c_size_t(0)
+    call("ldpc_make_G_device_workspace_bytes", code.handle, C.byref(n))
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    ws = torch.empty(max(int(n.value), 256), dtype=torch.uint8, device=dev)
+    call("ldpc_make_G_device", code.handle, _ptr(ws), C.c_size_t(ws.numel()), _stream(stream))
+    return code
+
+
 def ldpc_code_query(code: Code) -> CodeInfo:
     info = CodeInfo()
     call("ldpc_code_query", code.handle, C.byref(info))

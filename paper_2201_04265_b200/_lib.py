@@ -15,7 +15,8 @@ LIB_PATH = os.path.join(_HERE, "libldpc_b200.so")
 
 # symbols declared in include/ldpc.h (a CPU test checks the two lists agree)
 EXPORTED = [
-    "ldpc_make_H", "ldpc_code_from_csr", "ldpc_code_from_alist", "ldpc_code_write_alist", "ldpc_make_G", "ldpc_code_query", "ldpc_code_copy_H",
+    "ldpc_make_H", "ldpc_code_from_csr", "ldpc_code_from_alist", "ldpc_code_write_alist", "ldpc_make_G",
+    "ldpc_make_G_device_workspace_bytes", "ldpc_make_G_device", "ldpc_code_query", "ldpc_code_copy_H",
     "ldpc_code_copy_csr", "ldpc_code_copy_perm", "ldpc_code_copy_P", "ldpc_code_bind_device",
     "ldpc_code_free", "ldpc_status_str", "ldpc_encode", "ldpc_decode_workspace_bytes", "ldpc_decode",
     "ldpc_decode_variant", "ldpc_decode_simulate",
@@ -57,6 +58,8 @@ def lib() -> C.CDLL:
             "ldpc_code_from_alist": [C.c_char_p, sz, vp],
             "ldpc_code_write_alist": [vp, C.c_char_p, sz, vp],
             "ldpc_make_G": [vp],
+            "ldpc_make_G_device_workspace_bytes": [vp, vp],
+            "ldpc_make_G_device": [vp, vp, sz, vp],
             "ldpc_code_query": [vp, vp],
             "ldpc_code_copy_H": [vp, vp],
             "ldpc_code_copy_csr": [vp, vp, vp],
