@@ -207,6 +207,143 @@ DeviceLayout compute_layout(const ldpc_code &c, bool with_G) {
     return L;
 }
 
+// Shared-memory bank balancing of the 16-bit band view (MODE 2 band kernel).
+// In the check phase a warp processes 32 consecutive band-b rows (positions
+// 32u .. 32u+31 of the concatenated band index, u any) and, for element j,
+// gathers L (and E, at a band-constant offset) of the rows' j-th variables:
+// one shared-memory instruction whose cost is the largest number of the 32
+// addresses in one bank (random Tanner-graph rows: 3.5 wavefronts on
+// average).  Neither the order of a band's rows nor the order of a row's wr
+// variables matters to the algorithm (E is stored at variable positions and a
+// check node is symmetric), so both are chosen here: rows are moved between a
+// band's 32-row windows to flatten each window's histogram of variable banks
+// (swap local search on sum (count - wr)^2), then each row's variables are
+// assigned to elements so that every element column of the window hits
+// distinct banks where possible (greedy + pairwise repair).  l16 holds 4 v per
+// (band, position, element); only its order changes.  Deterministic.
+void bank_balance_rows(int32_t n, int32_t wc, int32_t wr, std::vector<uint16_t> &l16) {
+    const int32_t mb = n / wr, NB = wc - 1;
+    if (wr > 32 || mb < 64) return;
+    SplitMix64 rng(0x9e3779b97f4a7c15ull ^ uint64_t(n));
+    auto bank = [](uint16_t off) { return int((off >> 2) & 31); };
+    for (int32_t b = 0; b < NB; ++b) {
+        uint16_t *band = l16.data() + size_t(b) * size_t(n);
+        // windows: 32-aligned blocks of the concatenated row index, clipped to this band
+        const int32_t base = b * mb;
+        std::vector<int32_t> wstart, wlen;
+        for (int32_t r = base; r < base + mb;) {
+            const int32_t end = std::min(base + mb, (r / 32 + 1) * 32);
+            wstart.push_back(r - base);
+            wlen.push_back(end - r);
+            r = end;
+        }
+        const int32_t nw = int32_t(wstart.size());
+        std::vector<int32_t> row_win(static_cast<size_t>(mb)), rows(static_cast<size_t>(mb));
+        for (int32_t w = 0; w < nw; ++w)
+            for (int32_t i = 0; i < wlen[size_t(w)]; ++i) row_win[size_t(wstart[size_t(w)] + i)] = w;
+        for (int32_t r = 0; r < mb; ++r) rows[size_t(r)] = r;
+        std::vector<int32_t> H(size_t(nw) * 32, 0);
+        for (int32_t r = 0; r < mb; ++r)
+            for (int32_t j = 0; j < wr; ++j) H[size_t(row_win[size_t(r)]) * 32 + bank(band[size_t(r) * wr + j])]++;
+        // target count per bank: wlen * wr / 32 (x32 to stay integral)
+        auto cost_of = [&](int32_t w, const int32_t *h) {
+            int64_t s = 0;
+            for (int q = 0; q < 32; ++q) {
+                const int64_t d = int64_t(h[q]) * 32 - int64_t(wlen[size_t(w)]) * wr;
+                s += d * d;
+            }
+            return s;
+        };
+        const int64_t attempts = int64_t(mb) * 200;
+        int32_t ha[32], hb[32];
+        for (int64_t t = 0; t < attempts; ++t) {
+            const int32_t r = int32_t(rng.next() % uint64_t(mb)), s = int32_t(rng.next() % uint64_t(mb));
+            const int32_t wa = row_win[size_t(r)], wb = row_win[size_t(s)];
+            if (wa == wb) continue;
+            std::copy(&H[size_t(wa) * 32], &H[size_t(wa) * 32] + 32, ha);
+            std::copy(&H[size_t(wb) * 32], &H[size_t(wb) * 32] + 32, hb);
+            const int64_t c0 = cost_of(wa, ha) + cost_of(wb, hb);
+            for (int32_t j = 0; j < wr; ++j) {
+                const int br = bank(band[size_t(r) * wr + j]), bs = bank(band[size_t(s) * wr + j]);
+                ha[br]--; ha[bs]++; hb[bs]--; hb[br]++;
+            }
+            const int64_t c1 = cost_of(wa, ha) + cost_of(wb, hb);
+            if (c1 < c0) {
+                std::copy(ha, ha + 32, &H[size_t(wa) * 32]);
+                std::copy(hb, hb + 32, &H[size_t(wb) * 32]);
+                row_win[size_t(r)] = wb;
+                row_win[size_t(s)] = wa;
+            }
+        }
+        // lay the rows out window by window; then order each row's elements
+        std::vector<std::vector<int32_t>> members(static_cast<size_t>(nw));
+        for (int32_t r = 0; r < mb; ++r) members[size_t(row_win[size_t(r)])].push_back(r);
+        std::vector<uint16_t> out(static_cast<size_t>(mb) * wr);
+        std::vector<int32_t> cnt(size_t(wr) * 32);
+        std::vector<uint16_t> el;
+        for (int32_t w = 0; w < nw; ++w) {
+            const auto &mem = members[size_t(w)];
+            std::fill(cnt.begin(), cnt.end(), 0);
+            uint16_t *dst = out.data() + size_t(wstart[size_t(w)]) * wr;
+            for (size_t i = 0; i < mem.size(); ++i) {
+                el.assign(band + size_t(mem[i]) * wr, band + size_t(mem[i]) * wr + wr);
+                // most constrained variables first (their bank is busiest)
+                std::sort(el.begin(), el.end(), [&](uint16_t x, uint16_t y) {
+                    int cx = 0, cy = 0;
+                    for (int32_t j = 0; j < wr; ++j) { cx += cnt[size_t(j) * 32 + bank(x)]; cy += cnt[size_t(j) * 32 + bank(y)]; }
+                    return cx > cy || (cx == cy && x < y);
+                });
+                uint32_t used = 0;
+                uint16_t *row = dst + i * wr;
+                for (uint16_t v : el) {
+                    int32_t best = -1, bc = 1 << 30;
+                    for (int32_t j = 0; j < wr; ++j)
+                        if (!(used >> j & 1u) && cnt[size_t(j) * 32 + bank(v)] < bc) { bc = cnt[size_t(j) * 32 + bank(v)]; best = j; }
+                    used |= 1u << best;
+                    row[best] = v;
+                    cnt[size_t(best) * 32 + bank(v)]++;
+                }
+            }
+            // repair: swap two elements of a row when it lowers the column conflicts
+            for (int pass = 0; pass < 8; ++pass) {
+                bool any = false;
+                for (size_t i = 0; i < mem.size(); ++i) {
+                    uint16_t *row = dst + i * wr;
+                    for (int32_t x = 0; x < wr; ++x)
+                        for (int32_t y = x + 1; y < wr; ++y) {
+                            const int bx = bank(row[x]), by = bank(row[y]);
+                            if (bx == by) continue;
+                            // conflicts = sum over columns of max(0, cnt - 1)
+                            const int before = (cnt[size_t(x) * 32 + bx] > 1) + (cnt[size_t(y) * 32 + by] > 1);
+                            const int after = (cnt[size_t(x) * 32 + by] >= 1) + (cnt[size_t(y) * 32 + bx] >= 1);
+                            if (after < before) {
+                                cnt[size_t(x) * 32 + bx]--; cnt[size_t(y) * 32 + by]--;
+                                cnt[size_t(x) * 32 + by]++; cnt[size_t(y) * 32 + bx]++;
+                                std::swap(row[x], row[y]);
+                                any = true;
+                            }
+                        }
+                }
+                if (!any) break;
+            }
+        }
+        std::copy(out.begin(), out.end(), band);
+        if (std::getenv("LDPC_DEBUG")) {
+            double tot = 0;
+            int nins = 0;
+            for (int32_t w = 0; w < nw; ++w)
+                for (int32_t j = 0; j < wr; ++j) {
+                    int h[32] = {0}, mx = 0;
+                    for (int32_t i = 0; i < wlen[size_t(w)]; ++i)
+                        mx = std::max(mx, ++h[bank(band[size_t(wstart[size_t(w)] + i) * wr + j])]);
+                    tot += mx;
+                    ++nins;
+                }
+            std::fprintf(stderr, "ldpc bank_balance: band %d: %.3f wavefronts per gather\n", b + 1, tot / nins);
+        }
+    }
+}
+
 // Message-segment tables of the exchange cluster kernel (spa_cluster.cu).
 // CTA q owns band rows [q mbq, (q+1) mbq) of every band and the variables
 // [q nq, (q+1) nq) of its band-0 rows.  With T = xband_threads(mbq) compute
@@ -674,6 +811,7 @@ ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, vo
         if (ok && n <= 16383) {
             l16.resize(lidx.size());
             for (size_t e = 0; e < lidx.size(); ++e) l16[e] = uint16_t(size_t(lidx[e]) - lbase);
+            if (!std::getenv("LDPC_NO_BANKOPT")) ldpc::bank_balance_rows(n, wc, code->wr, l16);
             ok = put(L.band_lidx16, l16.data(), sizeof(uint16_t) * l16.size());
         }
         const int C = ldpc::band_cluster_size(n, wc, code->wr);
