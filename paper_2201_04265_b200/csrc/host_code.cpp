@@ -219,15 +219,17 @@ DeviceLayout compute_layout(const ldpc_code &c, bool with_G) {
 // band's 32-row windows to flatten each window's histogram of variable banks
 // (swap local search on sum (count - wr)^2), then each row's variables are
 // assigned to elements so that every element column of the window hits
-// distinct banks where possible (greedy + pairwise repair).  l16 holds 4 v per
-// (band, position, element); only its order changes.  Deterministic.
-void bank_balance_rows(int32_t n, int32_t wc, int32_t wr, std::vector<uint16_t> &l16) {
+// distinct banks where possible (greedy + pairwise repair).  rel holds 4 v per
+// (band, position, element) (the byte offset of L_v relative to L; a
+// band-constant shift does not change conflicts); only its order changes.
+// Deterministic.
+void bank_balance_rows(int32_t n, int32_t wc, int32_t wr, std::vector<int32_t> &rel) {
     const int32_t mb = n / wr, NB = wc - 1;
     if (wr > 32 || mb < 64) return;
     SplitMix64 rng(0x9e3779b97f4a7c15ull ^ uint64_t(n));
-    auto bank = [](uint16_t off) { return int((off >> 2) & 31); };
+    auto bank = [](int32_t off) { return int((off >> 2) & 31); };
     for (int32_t b = 0; b < NB; ++b) {
-        uint16_t *band = l16.data() + size_t(b) * size_t(n);
+        int32_t *band = rel.data() + size_t(b) * size_t(n);
         // windows: 32-aligned blocks of the concatenated row index, clipped to this band
         const int32_t base = b * mb;
         std::vector<int32_t> wstart, wlen;
@@ -278,24 +280,24 @@ void bank_balance_rows(int32_t n, int32_t wc, int32_t wr, std::vector<uint16_t> 
         // lay the rows out window by window; then order each row's elements
         std::vector<std::vector<int32_t>> members(static_cast<size_t>(nw));
         for (int32_t r = 0; r < mb; ++r) members[size_t(row_win[size_t(r)])].push_back(r);
-        std::vector<uint16_t> out(static_cast<size_t>(mb) * wr);
+        std::vector<int32_t> out(static_cast<size_t>(mb) * wr);
         std::vector<int32_t> cnt(size_t(wr) * 32);
-        std::vector<uint16_t> el;
+        std::vector<int32_t> el;
         for (int32_t w = 0; w < nw; ++w) {
             const auto &mem = members[size_t(w)];
             std::fill(cnt.begin(), cnt.end(), 0);
-            uint16_t *dst = out.data() + size_t(wstart[size_t(w)]) * wr;
+            int32_t *dst = out.data() + size_t(wstart[size_t(w)]) * wr;
             for (size_t i = 0; i < mem.size(); ++i) {
                 el.assign(band + size_t(mem[i]) * wr, band + size_t(mem[i]) * wr + wr);
                 // most constrained variables first (their bank is busiest)
-                std::sort(el.begin(), el.end(), [&](uint16_t x, uint16_t y) {
+                std::sort(el.begin(), el.end(), [&](int32_t x, int32_t y) {
                     int cx = 0, cy = 0;
                     for (int32_t j = 0; j < wr; ++j) { cx += cnt[size_t(j) * 32 + bank(x)]; cy += cnt[size_t(j) * 32 + bank(y)]; }
                     return cx > cy || (cx == cy && x < y);
                 });
                 uint32_t used = 0;
-                uint16_t *row = dst + i * wr;
-                for (uint16_t v : el) {
+                int32_t *row = dst + i * wr;
+                for (int32_t v : el) {
                     int32_t best = -1, bc = 1 << 30;
                     for (int32_t j = 0; j < wr; ++j)
                         if (!(used >> j & 1u) && cnt[size_t(j) * 32 + bank(v)] < bc) { bc = cnt[size_t(j) * 32 + bank(v)]; best = j; }
@@ -308,7 +310,7 @@ void bank_balance_rows(int32_t n, int32_t wc, int32_t wr, std::vector<uint16_t> 
             for (int pass = 0; pass < 8; ++pass) {
                 bool any = false;
                 for (size_t i = 0; i < mem.size(); ++i) {
-                    uint16_t *row = dst + i * wr;
+                    int32_t *row = dst + i * wr;
                     for (int32_t x = 0; x < wr; ++x)
                         for (int32_t y = x + 1; y < wr; ++y) {
                             const int bx = bank(row[x]), by = bank(row[y]);
@@ -799,19 +801,25 @@ ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, vo
         const size_t lbase = ldpc::band_L_byte_offset(n, wc);
         lidx.resize(size_t(wc - 1) * size_t(n));
         vpos.resize(size_t(wc - 1) * size_t(n));
+        // (row, element) order of every band >= 1: bank-balanced for the
+        // check phase's gathers (ldpc::bank_balance_rows); E's check-major
+        // slot (band_vpos) and both offset views follow that order
+        std::vector<int32_t> rel(size_t(wc - 1) * size_t(n));
+        for (int32_t b = 1; b < wc; ++b)
+            for (int32_t p = 0; p < n; ++p) rel[size_t(b - 1) * n + p] = 4 * code->col_idx[size_t(b) * n + p];
+        if (!std::getenv("LDPC_NO_BANKOPT")) ldpc::bank_balance_rows(n, wc, code->wr, rel);
         for (int32_t b = 1; b < wc; ++b)
             for (int32_t p = 0; p < n; ++p) {
-                const int32_t v = code->col_idx[size_t(b) * n + p];
-                lidx[size_t(b - 1) * n + p] = int32_t(lbase + 4 * size_t(v));
-                vpos[size_t(v) * (wc - 1) + (b - 1)] = int32_t(4 * (size_t(b - 1) * n + p));
+                const int32_t x = rel[size_t(b - 1) * n + p];
+                lidx[size_t(b - 1) * n + p] = int32_t(lbase) + x;
+                vpos[size_t(x / 4) * (wc - 1) + (b - 1)] = int32_t(4 * (size_t(b - 1) * n + p));
             }
         ok = put(L.band_lidx, lidx.data(), sizeof(int32_t) * lidx.size()) &&
              put(L.band_vpos, vpos.data(), sizeof(int32_t) * vpos.size());
         std::vector<uint16_t> l16;
         if (ok && n <= 16383) {
-            l16.resize(lidx.size());
-            for (size_t e = 0; e < lidx.size(); ++e) l16[e] = uint16_t(size_t(lidx[e]) - lbase);
-            if (!std::getenv("LDPC_NO_BANKOPT")) ldpc::bank_balance_rows(n, wc, code->wr, l16);
+            l16.resize(rel.size());
+            for (size_t e = 0; e < rel.size(); ++e) l16[e] = uint16_t(rel[e]);
             ok = put(L.band_lidx16, l16.data(), sizeof(uint16_t) * l16.size());
         }
         const int C = ldpc::band_cluster_size(n, wc, code->wr);
