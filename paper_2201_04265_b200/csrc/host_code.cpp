@@ -223,11 +223,125 @@ DeviceLayout compute_layout(const ldpc_code &c, bool with_G) {
 // (band, position, element) (the byte offset of L_v relative to L; a
 // band-constant shift does not change conflicts); only its order changes.
 // Deterministic.
+// Core of the balancing: rows[0 .. nrows*wr) (byte offsets; bank = offset/4
+// mod 32) are partitioned into the given windows (start, len) of consecutive
+// row positions.  Rows are moved between windows to flatten each window's
+// bank histogram, then each row's elements are ordered so that every element
+// column of a window hits distinct banks where possible.
+void balance_windows(int32_t *rowsv, int32_t nrows, int32_t wr, const std::vector<int32_t> &wstart,
+                     const std::vector<int32_t> &wlen, SplitMix64 &rng) {
+    auto bank = [](int32_t off) { return int((off >> 2) & 31); };
+    const int32_t nw = int32_t(wstart.size());
+    if (nw < 1 || nrows < 1) return;
+    std::vector<int32_t> row_win(static_cast<size_t>(nrows));
+    for (int32_t w = 0; w < nw; ++w)
+        for (int32_t i = 0; i < wlen[size_t(w)]; ++i) row_win[size_t(wstart[size_t(w)] + i)] = w;
+    std::vector<int32_t> H(size_t(nw) * 32, 0);
+    for (int32_t r = 0; r < nrows; ++r)
+        for (int32_t j = 0; j < wr; ++j) H[size_t(row_win[size_t(r)]) * 32 + bank(rowsv[size_t(r) * wr + j])]++;
+    auto cost_of = [&](int32_t w, const int32_t *h) {
+        int64_t s = 0;
+        for (int q = 0; q < 32; ++q) {
+            const int64_t d = int64_t(h[q]) * 32 - int64_t(wlen[size_t(w)]) * wr;
+            s += d * d;
+        }
+        return s;
+    };
+    if (nw > 1) {
+        const int64_t attempts = int64_t(nrows) * 200;
+        int32_t ha[32], hb[32];
+        for (int64_t t = 0; t < attempts; ++t) {
+            const int32_t r = int32_t(rng.next() % uint64_t(nrows)), s = int32_t(rng.next() % uint64_t(nrows));
+            const int32_t wa = row_win[size_t(r)], wb = row_win[size_t(s)];
+            if (wa == wb) continue;
+            std::copy(&H[size_t(wa) * 32], &H[size_t(wa) * 32] + 32, ha);
+            std::copy(&H[size_t(wb) * 32], &H[size_t(wb) * 32] + 32, hb);
+            const int64_t c0 = cost_of(wa, ha) + cost_of(wb, hb);
+            for (int32_t j = 0; j < wr; ++j) {
+                const int br = bank(rowsv[size_t(r) * wr + j]), bs = bank(rowsv[size_t(s) * wr + j]);
+                ha[br]--; ha[bs]++; hb[bs]--; hb[br]++;
+            }
+            const int64_t c1 = cost_of(wa, ha) + cost_of(wb, hb);
+            if (c1 < c0) {
+                std::copy(ha, ha + 32, &H[size_t(wa) * 32]);
+                std::copy(hb, hb + 32, &H[size_t(wb) * 32]);
+                row_win[size_t(r)] = wb;
+                row_win[size_t(s)] = wa;
+            }
+        }
+    }
+    std::vector<std::vector<int32_t>> members(static_cast<size_t>(nw));
+    for (int32_t r = 0; r < nrows; ++r) members[size_t(row_win[size_t(r)])].push_back(r);
+    std::vector<int32_t> out(static_cast<size_t>(nrows) * wr);
+    std::vector<int32_t> cnt(size_t(wr) * 32);
+    std::vector<int32_t> el;
+    for (int32_t w = 0; w < nw; ++w) {
+        const auto &mem = members[size_t(w)];
+        std::fill(cnt.begin(), cnt.end(), 0);
+        int32_t *dst = out.data() + size_t(wstart[size_t(w)]) * wr;
+        for (size_t i = 0; i < mem.size(); ++i) {
+            el.assign(rowsv + size_t(mem[i]) * wr, rowsv + size_t(mem[i]) * wr + wr);
+            // most constrained variables first (their bank is busiest)
+            std::sort(el.begin(), el.end(), [&](int32_t x, int32_t y) {
+                int cx = 0, cy = 0;
+                for (int32_t j = 0; j < wr; ++j) { cx += cnt[size_t(j) * 32 + bank(x)]; cy += cnt[size_t(j) * 32 + bank(y)]; }
+                return cx > cy || (cx == cy && x < y);
+            });
+            uint32_t used = 0;
+            int32_t *row = dst + i * wr;
+            for (int32_t v : el) {
+                int32_t best = -1, bc = 1 << 30;
+                for (int32_t j = 0; j < wr; ++j)
+                    if (!(used >> j & 1u) && cnt[size_t(j) * 32 + bank(v)] < bc) { bc = cnt[size_t(j) * 32 + bank(v)]; best = j; }
+                used |= 1u << best;
+                row[best] = v;
+                cnt[size_t(best) * 32 + bank(v)]++;
+            }
+        }
+        // repair: swap two elements of a row when it lowers the column conflicts
+        for (int pass = 0; pass < 8; ++pass) {
+            bool any = false;
+            for (size_t i = 0; i < mem.size(); ++i) {
+                int32_t *row = dst + i * wr;
+                for (int32_t x = 0; x < wr; ++x)
+                    for (int32_t y = x + 1; y < wr; ++y) {
+                        const int bx = bank(row[x]), by = bank(row[y]);
+                        if (bx == by) continue;
+                        const int before = (cnt[size_t(x) * 32 + bx] > 1) + (cnt[size_t(y) * 32 + by] > 1);
+                        const int after = (cnt[size_t(x) * 32 + by] >= 1) + (cnt[size_t(y) * 32 + bx] >= 1);
+                        if (after < before) {
+                            cnt[size_t(x) * 32 + bx]--; cnt[size_t(y) * 32 + by]--;
+                            cnt[size_t(x) * 32 + by]++; cnt[size_t(y) * 32 + bx]++;
+                            std::swap(row[x], row[y]);
+                            any = true;
+                        }
+                    }
+            }
+            if (!any) break;
+        }
+    }
+    std::copy(out.begin(), out.end(), rowsv);
+}
+
+// Mean wavefronts per gather of a balanced (or not) row array (debug).
+double window_wavefronts(const int32_t *rowsv, int32_t wr, const std::vector<int32_t> &wstart,
+                         const std::vector<int32_t> &wlen) {
+    double tot = 0;
+    int nins = 0;
+    for (size_t w = 0; w < wstart.size(); ++w)
+        for (int32_t j = 0; j < wr; ++j) {
+            int h[32] = {0}, mx = 0;
+            for (int32_t i = 0; i < wlen[w]; ++i) mx = std::max(mx, ++h[(rowsv[size_t(wstart[w] + i) * wr + j] >> 2) & 31]);
+            tot += mx;
+            ++nins;
+        }
+    return nins ? tot / nins : 0.0;
+}
+
 void bank_balance_rows(int32_t n, int32_t wc, int32_t wr, std::vector<int32_t> &rel) {
     const int32_t mb = n / wr, NB = wc - 1;
     if (wr > 32 || mb < 64) return;
     SplitMix64 rng(0x9e3779b97f4a7c15ull ^ uint64_t(n));
-    auto bank = [](int32_t off) { return int((off >> 2) & 31); };
     for (int32_t b = 0; b < NB; ++b) {
         int32_t *band = rel.data() + size_t(b) * size_t(n);
         // windows: 32-aligned blocks of the concatenated row index, clipped to this band
@@ -239,110 +353,10 @@ void bank_balance_rows(int32_t n, int32_t wc, int32_t wr, std::vector<int32_t> &
             wlen.push_back(end - r);
             r = end;
         }
-        const int32_t nw = int32_t(wstart.size());
-        std::vector<int32_t> row_win(static_cast<size_t>(mb)), rows(static_cast<size_t>(mb));
-        for (int32_t w = 0; w < nw; ++w)
-            for (int32_t i = 0; i < wlen[size_t(w)]; ++i) row_win[size_t(wstart[size_t(w)] + i)] = w;
-        for (int32_t r = 0; r < mb; ++r) rows[size_t(r)] = r;
-        std::vector<int32_t> H(size_t(nw) * 32, 0);
-        for (int32_t r = 0; r < mb; ++r)
-            for (int32_t j = 0; j < wr; ++j) H[size_t(row_win[size_t(r)]) * 32 + bank(band[size_t(r) * wr + j])]++;
-        // target count per bank: wlen * wr / 32 (x32 to stay integral)
-        auto cost_of = [&](int32_t w, const int32_t *h) {
-            int64_t s = 0;
-            for (int q = 0; q < 32; ++q) {
-                const int64_t d = int64_t(h[q]) * 32 - int64_t(wlen[size_t(w)]) * wr;
-                s += d * d;
-            }
-            return s;
-        };
-        const int64_t attempts = int64_t(mb) * 200;
-        int32_t ha[32], hb[32];
-        for (int64_t t = 0; t < attempts; ++t) {
-            const int32_t r = int32_t(rng.next() % uint64_t(mb)), s = int32_t(rng.next() % uint64_t(mb));
-            const int32_t wa = row_win[size_t(r)], wb = row_win[size_t(s)];
-            if (wa == wb) continue;
-            std::copy(&H[size_t(wa) * 32], &H[size_t(wa) * 32] + 32, ha);
-            std::copy(&H[size_t(wb) * 32], &H[size_t(wb) * 32] + 32, hb);
-            const int64_t c0 = cost_of(wa, ha) + cost_of(wb, hb);
-            for (int32_t j = 0; j < wr; ++j) {
-                const int br = bank(band[size_t(r) * wr + j]), bs = bank(band[size_t(s) * wr + j]);
-                ha[br]--; ha[bs]++; hb[bs]--; hb[br]++;
-            }
-            const int64_t c1 = cost_of(wa, ha) + cost_of(wb, hb);
-            if (c1 < c0) {
-                std::copy(ha, ha + 32, &H[size_t(wa) * 32]);
-                std::copy(hb, hb + 32, &H[size_t(wb) * 32]);
-                row_win[size_t(r)] = wb;
-                row_win[size_t(s)] = wa;
-            }
-        }
-        // lay the rows out window by window; then order each row's elements
-        std::vector<std::vector<int32_t>> members(static_cast<size_t>(nw));
-        for (int32_t r = 0; r < mb; ++r) members[size_t(row_win[size_t(r)])].push_back(r);
-        std::vector<int32_t> out(static_cast<size_t>(mb) * wr);
-        std::vector<int32_t> cnt(size_t(wr) * 32);
-        std::vector<int32_t> el;
-        for (int32_t w = 0; w < nw; ++w) {
-            const auto &mem = members[size_t(w)];
-            std::fill(cnt.begin(), cnt.end(), 0);
-            int32_t *dst = out.data() + size_t(wstart[size_t(w)]) * wr;
-            for (size_t i = 0; i < mem.size(); ++i) {
-                el.assign(band + size_t(mem[i]) * wr, band + size_t(mem[i]) * wr + wr);
-                // most constrained variables first (their bank is busiest)
-                std::sort(el.begin(), el.end(), [&](int32_t x, int32_t y) {
-                    int cx = 0, cy = 0;
-                    for (int32_t j = 0; j < wr; ++j) { cx += cnt[size_t(j) * 32 + bank(x)]; cy += cnt[size_t(j) * 32 + bank(y)]; }
-                    return cx > cy || (cx == cy && x < y);
-                });
-                uint32_t used = 0;
-                int32_t *row = dst + i * wr;
-                for (int32_t v : el) {
-                    int32_t best = -1, bc = 1 << 30;
-                    for (int32_t j = 0; j < wr; ++j)
-                        if (!(used >> j & 1u) && cnt[size_t(j) * 32 + bank(v)] < bc) { bc = cnt[size_t(j) * 32 + bank(v)]; best = j; }
-                    used |= 1u << best;
-                    row[best] = v;
-                    cnt[size_t(best) * 32 + bank(v)]++;
-                }
-            }
-            // repair: swap two elements of a row when it lowers the column conflicts
-            for (int pass = 0; pass < 8; ++pass) {
-                bool any = false;
-                for (size_t i = 0; i < mem.size(); ++i) {
-                    int32_t *row = dst + i * wr;
-                    for (int32_t x = 0; x < wr; ++x)
-                        for (int32_t y = x + 1; y < wr; ++y) {
-                            const int bx = bank(row[x]), by = bank(row[y]);
-                            if (bx == by) continue;
-                            // conflicts = sum over columns of max(0, cnt - 1)
-                            const int before = (cnt[size_t(x) * 32 + bx] > 1) + (cnt[size_t(y) * 32 + by] > 1);
-                            const int after = (cnt[size_t(x) * 32 + by] >= 1) + (cnt[size_t(y) * 32 + bx] >= 1);
-                            if (after < before) {
-                                cnt[size_t(x) * 32 + bx]--; cnt[size_t(y) * 32 + by]--;
-                                cnt[size_t(x) * 32 + by]++; cnt[size_t(y) * 32 + bx]++;
-                                std::swap(row[x], row[y]);
-                                any = true;
-                            }
-                        }
-                }
-                if (!any) break;
-            }
-        }
-        std::copy(out.begin(), out.end(), band);
-        if (std::getenv("LDPC_DEBUG")) {
-            double tot = 0;
-            int nins = 0;
-            for (int32_t w = 0; w < nw; ++w)
-                for (int32_t j = 0; j < wr; ++j) {
-                    int h[32] = {0}, mx = 0;
-                    for (int32_t i = 0; i < wlen[size_t(w)]; ++i)
-                        mx = std::max(mx, ++h[bank(band[size_t(wstart[size_t(w)] + i) * wr + j])]);
-                    tot += mx;
-                    ++nins;
-                }
-            std::fprintf(stderr, "ldpc bank_balance: band %d: %.3f wavefronts per gather\n", b + 1, tot / nins);
-        }
+        balance_windows(band, mb, wr, wstart, wlen, rng);
+        if (std::getenv("LDPC_DEBUG"))
+            std::fprintf(stderr, "ldpc bank_balance: band %d: %.3f wavefronts per gather\n", b + 1,
+                         window_wavefronts(band, wr, wstart, wlen));
     }
 }
 
@@ -412,6 +426,36 @@ int32_t xband_tables(const ldpc_code &c, int C, std::vector<uint16_t> &ridx, std
             ridx[size_t(b) * n + p] = uint16_t(rowOff[k] + 4 * r);
             sidx[size_t(v) * NB + b] = uint16_t(varOff[k] + 4 * r);
         }
+    // Bank balancing of the C-phase gathers (see balance_windows): a CTA's
+    // band-b rows of one row step (one C chunk: their segments are fixed) may
+    // be processed in any order and a row's slots listed in any order, so both
+    // are chosen to spread each warp's 32 row-region addresses over the banks.
+    if (!std::getenv("LDPC_NO_BANKOPT")) {
+        SplitMix64 rng(0x7f4a7c159e3779b9ull ^ uint64_t(n) ^ (uint64_t(C) << 32));
+        std::vector<int32_t> rows;
+        double before = 0, after = 0;
+        int nchunks = 0;
+        for (int32_t d = 0; d < C; ++d)
+            for (int32_t b = 0; b < NB; ++b)
+                for (int32_t k0 = 0; k0 < mbq; k0 += T) {
+                    const int32_t nr = std::min(T, mbq - k0);
+                    uint16_t *base = ridx.data() + size_t(b) * n + size_t(d * mbq + k0) * wr;
+                    rows.assign(base, base + size_t(nr) * wr);
+                    std::vector<int32_t> wstart, wlen;
+                    for (int32_t r = 0; r < nr; r += 32) {
+                        wstart.push_back(r);
+                        wlen.push_back(std::min(32, nr - r));
+                    }
+                    if (std::getenv("LDPC_DEBUG")) before += window_wavefronts(rows.data(), wr, wstart, wlen);
+                    balance_windows(rows.data(), nr, wr, wstart, wlen, rng);
+                    if (std::getenv("LDPC_DEBUG")) after += window_wavefronts(rows.data(), wr, wstart, wlen);
+                    ++nchunks;
+                    for (size_t i = 0; i < rows.size(); ++i) base[i] = uint16_t(rows[i]);
+                }
+        if (std::getenv("LDPC_DEBUG"))
+            std::fprintf(stderr, "ldpc xband bank_balance: C-phase %.3f -> %.3f wavefronts per gather\n",
+                         before / std::max(nchunks, 1), after / std::max(nchunks, 1));
+    }
     return cap;
 }
 }  // namespace ldpc
