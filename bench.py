@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--config", default="C4", choices=sorted(W.ALL))
     ap.add_argument("--frames", type=int, default=0, help="override frames per GPU per step")
     ap.add_argument("--e2e-frames", type=int, default=0, help="cap on e2e frames per step (0 = the batch)")
+    ap.add_argument("--e2e-chunk", type=int, default=8192, help="frames per H2D/compute/D2H pipeline chunk (e2e)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--eager", action="store_true", help="launch the step's kernels eagerly instead of replaying a CUDA graph")
@@ -523,7 +524,7 @@ def e2e_measure(L, code, wl, args, dev, frame0, k, n, kw, nw, world, frames):
     F = frames
     if args.e2e_frames:
         F = min(F, args.e2e_frames)
-    Fc = min(F, 16384)                       # pipeline chunk
+    Fc = min(F, args.e2e_chunk)              # pipeline chunk
     nchunks = (F + Fc - 1) // Fc
     try:
         h_info = torch.empty((F, kw), dtype=torch.int32, pin_memory=True)

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstddef>
+#include <cstdlib>
 #include <cstdint>
 #include <vector>
 
@@ -127,6 +128,10 @@ inline bool xband_fits(int32_t n, int32_t wc, int32_t wr, int C) {
 inline bool band_frame_fits_sm(int32_t n, int32_t wc) { return size_t(wc) * size_t(n) * 4 + 1024 <= 227 * 1024; }
 inline int xband_cluster_size(int32_t n, int32_t wc, int32_t wr) {
     if (wc < 2 || wr < 1 || n % wr) return 0;
+    if (const char *e = std::getenv("LDPC_XBAND_C")) {          // experiments: force a cluster size
+        const int C = std::atoi(e);
+        return (C >= 2 && C <= 16 && xband_fits(n, wc, wr, C)) ? C : 0;
+    }
     if (band_frame_fits_sm(n, wc)) {
         for (int C = 8; C >= 2; C /= 2)
             if ((n / wr) % C == 0 && n / wr / C >= 64 && xband_fits(n, wc, wr, C)) return C;
