@@ -43,7 +43,9 @@ __device__ __forceinline__ bool cta_sync_or(bool p) { return __syncthreads_or(p 
 // exactly as ldpc_channel does (channel_common.cuh) instead of loading it, and
 // the epilogue accumulates the counters of ldpc_count_errors per CTA (flushed
 // with six atomics when the CTA runs out of frames).
-template <int WR, int WC, int B0, bool ET, int MODE, int NFIX = 0, bool GEN = false>
+// RPRE: band-0 rows whose R is prefetched before the check->variable barrier
+// (only when R lives in global memory).
+template <int WR, int WC, int B0, bool ET, int MODE, int NFIX = 0, bool GEN = false, int RPRE = 0>
 __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const BandArgs a) {
     constexpr bool VM = MODE >= 1, L16 = MODE == 2;
     extern __shared__ __align__(16) char smem[];
@@ -174,6 +176,18 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
                     }
                 }
             }
+            // R of this thread's first band-0 rows, loaded before the barrier so its
+            // latency (an L2-resident slot when R does not fit shared memory)
+            // overlaps the barrier wait instead of opening the variable phase
+            constexpr int RP = B0 < RPRE ? B0 : RPRE;
+            float rpre[RP > 0 ? RP : 1][WR];
+            if (RP > 0 && !r_in_smem) {
+#pragma unroll
+                for (int k = 0; k < RP; ++k) {
+                    const int r = tt + k * S;
+                    if (tt < S && r < mb) lds_row<WR>(reinterpret_cast<const char *>(Rs), uint32_t(r) * WR * 4u, rpre[k]);
+                }
+            }
             if (ET) {
                 const bool any = cta_sync_or(synd != 0);
                 if (t > 1 && !any) {      // z^{t-1} has zero syndrome: stop (reading c6)
@@ -190,7 +204,12 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
                 const int r = tt + k * S;
                 if (tt < S && r < mb) {
                     float rv[WR], lv[WR];
-                    lds_row<WR>(reinterpret_cast<const char *>(Rs), uint32_t(r) * WR * 4u, rv);
+                    if (k < RP && !r_in_smem) {
+#pragma unroll
+                        for (int j = 0; j < WR; ++j) rv[j] = rpre[k < RP ? k : 0][j];
+                    } else {
+                        lds_row<WR>(reinterpret_cast<const char *>(Rs), uint32_t(r) * WR * 4u, rv);
+                    }
                     if (VM) {
                         // this row's variables are contiguous in every band's E_b
 #pragma unroll

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "band_common.cuh"
 #include "ldpc_internal.h"
@@ -30,7 +31,18 @@ void *et_pair(bool et) {
 //   on B200 against NFIX = 0: C2 +2.6, C4 +2.9, C3-R3/4 +0.7, Table I R1/4
 //   (100k frames) +1.3 points of the SFU roofline; C3 (3,4) -0.7 (left out).
 void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode) {
-    if (wc == 3 && wr == 6 && n == 16200 && b0 == 3 && mode == 2) return et_pair<6, 3, 3, 2, 16200>(et);
+    if (wc == 3 && wr == 6 && n == 16200 && b0 == 3 && mode == 2) {
+        // R of 2 of the 3 band-0 rows prefetched before the check->variable
+        // barrier (RPRE; measured on B200: 0 rows 65.8%, 1 67.2%, 2 68.2%,
+        // 3 66.8% (spills) of the SFU roofline); LDPC_RPRE=0/1 for A/B
+        const char *e = std::getenv("LDPC_RPRE");
+        const int rp = e ? std::atoi(e) : 2;
+        if (rp == 1) return et ? reinterpret_cast<void *>(&band_kernel<6, 3, 3, true, 2, 16200, false, 1>)
+                               : reinterpret_cast<void *>(&band_kernel<6, 3, 3, false, 2, 16200, false, 1>);
+        if (rp == 2) return et ? reinterpret_cast<void *>(&band_kernel<6, 3, 3, true, 2, 16200, false, 2>)
+                               : reinterpret_cast<void *>(&band_kernel<6, 3, 3, false, 2, 16200, false, 2>);
+        return et_pair<6, 3, 3, 2, 16200>(et);
+    }
     if (wc == 3 && wr == 6 && n == 1008 && b0 == 1 && mode == 0) return et_pair<6, 3, 1, 0, 1008>(et);
     if (wc == 3 && n == 3996 && b0 == 1 && mode == 0) {
         if (wr == 6) return et_pair<6, 3, 1, 0, 3996>(et);
