@@ -5,6 +5,10 @@
 // translation unit.
 #pragma once
 
+#ifndef BAND_FUSE0
+#define BAND_FUSE0 true
+#endif
+
 struct BandArgs {
     DeviceCode code;
     const float *llr;
@@ -47,6 +51,9 @@ __device__ __forceinline__ bool cta_sync_or(bool p) { return __syncthreads_or(p 
 // (only when R lives in global memory).
 template <int WR, int WC, int B0, bool ET, int MODE, int NFIX = 0, bool GEN = false, int RPRE = 0>
 __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const BandArgs a) {
+    // measured on B200: +1.1 points on C4 (MODE 2), +0.8..1.3 on wr = 12 codes,
+    // -2..3 on check-major wr = 4 / 6 codes (C3 R1/4, R1/2)
+    constexpr bool FUSE0 = BAND_FUSE0 && (MODE == 2 || WR >= 12);
     constexpr bool VM = MODE >= 1, L16 = MODE == 2;
     extern __shared__ __align__(16) char smem[];
     __shared__ long long s_frame;
@@ -114,11 +121,28 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
 
         int32_t iters = a.max_iter;
         bool stopped = false;
-        for (int t = 1; t <= a.max_iter; ++t) {
-            // ---- a3: check-node phase (and syndrome of z^{t-1} when ET)
-            uint32_t synd = 0;
+        // Band-0 checks read only their own row's L, which the same thread has
+        // just produced in the variable phase: the band-0 check of iteration
+        // t+1 runs at the end of variable phase t from registers (FUSE0), and
+        // the one of t = 1 here, from L = R.  Same rows per warp, same inputs:
+        // results identical to running them in the check phase.
+        uint32_t synd0 = 0;            // ET: band-0 rows' syndrome bits of z^{t-1}
+        if constexpr (FUSE0) {
 #pragma unroll
             for (int k = 0; k < B0; ++k) {
+                const int r = tt + k * S;
+                if (tt < S && r < mb) {
+                    float x[WR];
+                    lds_row<WR>(smem, lbase + uint32_t(r) * WR * 4u, x);
+                    check_row<WR, !ET>(x, e0[k]);
+                }
+            }
+        }
+        for (int t = 1; t <= a.max_iter; ++t) {
+            // ---- a3: check-node phase (and syndrome of z^{t-1} when ET)
+            uint32_t synd = FUSE0 ? synd0 : 0u;
+#pragma unroll
+            for (int k = 0; k < (FUSE0 ? 0 : B0); ++k) {
                 const int r = tt + k * S;
                 if (tt < S && r < mb) {
                     float lv[WR], x[WR];
@@ -199,6 +223,7 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
                 __syncthreads();
             }
             // ---- a4/a5: variable-node phase, Eq. 7 (owners of band-0 rows)
+            synd0 = 0;
 #pragma unroll
             for (int k = 0; k < B0; ++k) {
                 const int r = tt + k * S;
@@ -233,6 +258,20 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
                         }
                     }
                     sts_row<WR>(smem, lbase + uint32_t(r) * WR * 4u, lv);
+                    if constexpr (FUSE0) {
+                        if (ET) {
+                            uint32_t rp = 0;      // this band-0 row's syndrome bit of z^t (Eq. 1)
+#pragma unroll
+                            for (int j = 0; j < WR; ++j) rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
+                            synd0 |= rp;
+                        }
+                        if (t < a.max_iter) {
+                            float x[WR];
+#pragma unroll
+                            for (int j = 0; j < WR; ++j) x[j] = lv[j] - e0[k][j];
+                            check_row<WR, !ET>(x, e0[k]);
+                        }
+                    }
                 }
             }
             __syncthreads();
