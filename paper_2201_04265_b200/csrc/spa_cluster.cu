@@ -313,6 +313,14 @@ __global__ void __launch_bounds__(MAXT, 1) xband_kernel(const XArgs a) {
                 }
                 // ---- V-phase t (a4/a5): L = R + sum E; L_vc over the E slots (L itself at t = T)
                 const bool last = t == a.max_iter;
+                // R does not depend on the exchange: its (L2) loads are issued
+                // before waiting for the E segments
+#pragma unroll
+                for (int h = 0; h < H; ++h) {
+                    const int r = tt + h * TW;
+                    if (r < mbq)
+                        lds_row<WR>(reinterpret_cast<const char *>(llr), uint32_t((int(q) * mbq + r) * WR) * 4u, lv[h]);
+                }
                 wait_var();
                 // Each chunk's L_vc go to the producer first; the band-0 checks
                 // (thread-local, x = L - E0) run afterwards, overlapping the transfer.
@@ -320,8 +328,6 @@ __global__ void __launch_bounds__(MAXT, 1) xband_kernel(const XArgs a) {
                 for (int h = 0; h < H; ++h) {
                     const int r = tt + h * TW;
                     if (r < mbq) {
-                        const int v0 = (int(q) * mbq + r) * WR;
-                        lds_row<WR>(reinterpret_cast<const char *>(llr), uint32_t(v0) * 4u, lv[h]);
                         const uint16_t *vt = vtab + size_t(r) * WR * NB;
                         uint32_t sl[WR * NB];
 #pragma unroll
