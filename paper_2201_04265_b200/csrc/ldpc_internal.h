@@ -68,6 +68,7 @@ struct DeviceCode {
     const int32_t *cband_lidx;
     const int32_t *cband_vpos;
     int32_t xcluster;              // C of the exchange cluster view (0: none)
+    int32_t xslots;                // 2: the view serves the two-slot kernel (xband2_kernel)
     int32_t xcap;                  // message region capacity (floats, multiple of 4)
     const uint16_t *xband_ridx;
     const uint16_t *xband_sidx;
@@ -126,6 +127,21 @@ inline bool xband_fits(int32_t n, int32_t wc, int32_t wr, int C) {
     return xband_smem_bytes(n, wc, wr, C, xband_capacity_bound(n, wc, wr, C)) + 1024 <= 227 * 1024;
 }
 inline bool band_frame_fits_sm(int32_t n, int32_t wc) { return size_t(wc) * size_t(n) * 4 + 1024 <= 227 * 1024; }
+// Two-slot exchange kernel (xband2_kernel): four regions + shared tables.
+inline size_t xband2_smem_bytes(int32_t n, int32_t wc, int32_t wr, int32_t C, int32_t cap) {
+    const size_t nq = size_t(n / wr / C) * size_t(wr);
+    return 4 * size_t(cap) * 4 + 2 * size_t(wc - 1) * nq * 2 + 16 + 2 * 8 * (3 + size_t(wc - 1)) + 2 * 4 * size_t(C);
+}
+// Frames larger than one SM whose 16-CTA view fits two frames per CTA with one
+// row per thread use 16-CTA clusters and two frames in flight (the (3,6)
+// instantiation; C5: 144 SMs instead of 120 and the exchange latency hidden).
+inline bool xband2_fits(int32_t n, int32_t wc, int32_t wr) {
+    constexpr int C = 16;
+    if (wc != 3 || wr != 6 || (n / wr) % C) return false;
+    const int32_t mbq = n / wr / C;
+    if (xband_rows_per_thread(mbq) != 1 || xband_threads(mbq) + 32 > 768) return false;
+    return xband2_smem_bytes(n, wc, wr, C, xband_capacity_bound(n, wc, wr, C)) + 1024 <= 227 * 1024;
+}
 inline int xband_cluster_size(int32_t n, int32_t wc, int32_t wr) {
     if (wc < 2 || wr < 1 || n % wr) return 0;
     if (const char *e = std::getenv("LDPC_XBAND_C")) {          // experiments: force a cluster size
@@ -137,6 +153,7 @@ inline int xband_cluster_size(int32_t n, int32_t wc, int32_t wr) {
             if ((n / wr) % C == 0 && n / wr / C >= 64 && xband_fits(n, wc, wr, C)) return C;
         return 0;
     }
+    if (!std::getenv("LDPC_XBAND_1SLOT") && xband2_fits(n, wc, wr) && xband_fits(n, wc, wr, 16)) return 16;
     for (int C = 2; C <= 16; C *= 2)
         if (xband_fits(n, wc, wr, C)) return C;
     return 0;

@@ -424,6 +424,289 @@ __global__ void __launch_bounds__(MAXT, 1) xband_kernel(const XArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Two frames in flight per cluster (slots 0 and 1; H = 1, e.g. 16-CTA
+// clusters on C5).  Each slot has its own VAR / ROW regions and barriers; the
+// slot tables are shared.  The compute warps alternate the slots' phases --
+// C(0), C(1), V(0), V(1) -- so one slot's segment exchange travels while the
+// other slot computes, hiding the exchange's fixed latency; the producer warp
+// ships the chunks in the same order.  Per slot the protocol and the safety
+// argument are those of xband_kernel.  Frames 2p and 2p+1 of cluster pair
+// index p run together; a lone last frame runs in slot 0 only.
+template <int WR, int WC, int C, int MAXT, int NFIX = 0>
+__global__ void __launch_bounds__(MAXT, 1) xband2_kernel(const XArgs a) {
+    extern __shared__ __align__(128) char smem[];
+    constexpr int NB = WC - 1, H = 1, NC = NB;
+    const DeviceCode &code = a.code;
+    const int n = NFIX ? NFIX : code.n, mb = NFIX ? NFIX / WR : code.mb, mbq = mb / C, nq = n / C;
+    const int TW = NFIX ? xband_threads(NFIX / WR / C) : int(blockDim.x) - 32, tt = threadIdx.x, lane = tt & 31;
+    const bool producer = tt >= TW;
+    const uint32_t cap_b = uint32_t(code.xcap) * 4u;
+    const uint32_t q = cluster_ctarank();
+    const int64_t cid = cluster_id_x(), ncl = ncluster_x();
+    char *varr[2] = {smem, smem + 2 * cap_b};
+    char *rowr[2] = {smem + cap_b, smem + 3 * cap_b};
+    uint16_t *vtab = reinterpret_cast<uint16_t *>(smem + 4 * cap_b);
+    uint16_t *rtab = vtab + size_t(nq) * NB;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + ((4 * cap_b + 4u * uint32_t(NB * nq) + 15u) & ~15u));
+    constexpr int NBAR = 2 + H + NC;                 // per slot: var, row, vchunk, cchunk[NC]
+    int *flags = reinterpret_cast<int *>(bars + 2 * NBAR);   // [2][C]
+    const uint32_t bar0 = saddr(bars);
+    auto vbar = [&](int sl) { return bar0 + 8u * uint32_t(sl * NBAR); };
+    auto rbar = [&](int sl) { return bar0 + 8u * uint32_t(sl * NBAR + 1); };
+    auto vchunk = [&](int sl) { return bar0 + 8u * uint32_t(sl * NBAR + 2); };
+    auto cchunk = [&](int sl, int c) { return bar0 + 8u * uint32_t(sl * NBAR + 3 + c); };
+    const int nkey = C * C * H * NC;
+    const int32_t *varOff = code.xband_seg, *rowOff = code.xband_seg + nkey, *sbytes = code.xband_seg + 2 * nkey;
+    auto key = [](int s, int d, int h, int c) { return ((s * C + d) * H + h) * NC + c; };
+    {
+        const uint32_t *src = reinterpret_cast<const uint32_t *>(code.xband_sidx + size_t(q) * nq * NB);
+        uint32_t *dst = reinterpret_cast<uint32_t *>(vtab);
+        for (int i = tt; i < nq * NB / 2; i += blockDim.x) dst[i] = __ldg(src + i);
+        for (int b = 0; b < NB; ++b) {
+            const uint32_t *rs = reinterpret_cast<const uint32_t *>(code.xband_ridx + size_t(b) * n + size_t(q) * mbq * WR);
+            uint32_t *rd = reinterpret_cast<uint32_t *>(rtab + size_t(b) * mbq * WR);
+            for (int i = tt; i < mbq * WR / 2; i += blockDim.x) rd[i] = __ldg(rs + i);
+        }
+    }
+    uint32_t rx_l = 0, rx_e = 0;
+    for (int s = 0; s < C; ++s)
+        for (int c = 0; c < NC; ++c) {
+            rx_l += uint32_t(__ldg(sbytes + key(s, q, 0, c)));
+            rx_e += uint32_t(__ldg(sbytes + key(q, s, 0, c)));
+        }
+    if (tt == 0) {
+        for (int sl = 0; sl < 2; ++sl) {
+            mbar_init(vbar(sl), 1);
+            mbar_init(rbar(sl), 1);
+            mbar_init(vchunk(sl), uint32_t(TW / 32));
+            for (int c = 0; c < NC; ++c) mbar_init(cchunk(sl, c), uint32_t(TW / 32));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int sl = 0; sl < 2; ++sl) {
+            mbar_arm(vbar(sl), rx_e);
+            mbar_arm(rbar(sl), rx_l);
+        }
+    }
+    cluster_sync_all();
+
+    auto chunk_done = [&](uint32_t bar) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_local(bar);
+    };
+    uint32_t nv[2] = {0, 0}, nc[2] = {0, 0};        // producer: chunk barrier phases per slot
+    uint32_t nl[2] = {0, 0}, ne[2] = {0, 0};        // compute: exchanges received per slot
+    auto ship_l = [&](int sl) {
+        mbar_wait(vchunk(sl), nv[sl] & 1u);
+        const uint32_t vs = saddr(varr[sl]), rs = saddr(rowr[sl]);
+        for (int i = lane; i < C * NC; i += 32) {
+            const int d = i / NC, c = i - d * NC;
+            const int k = key(int(q), d, 0, c);
+            const uint32_t nbytes = uint32_t(__ldg(sbytes + k));
+            if (nbytes)
+                bulk_s2c(mapa_u32(rs + uint32_t(__ldg(rowOff + k)), uint32_t(d)), vs + uint32_t(__ldg(varOff + k)), nbytes,
+                         mapa_u32(rbar(sl), uint32_t(d)));
+        }
+        ++nv[sl];
+    };
+    auto ship_e = [&](int sl, int c) {
+        mbar_wait(cchunk(sl, c), nc[sl] & 1u);
+        const uint32_t vs = saddr(varr[sl]), rs = saddr(rowr[sl]);
+        if (lane < C) {
+            const int s = lane;
+            const int k = key(s, int(q), 0, c);
+            const uint32_t nbytes = uint32_t(__ldg(sbytes + k));
+            if (nbytes)
+                bulk_s2c(mapa_u32(vs + uint32_t(__ldg(varOff + k)), uint32_t(s)), rs + uint32_t(__ldg(rowOff + k)), nbytes,
+                         mapa_u32(vbar(sl), uint32_t(s)));
+        }
+        if (c == NC - 1) ++nc[sl];
+    };
+    auto wait_row = [&](int sl) {
+        mbar_wait(rbar(sl), nl[sl] & 1u);
+        if (tt == 0) mbar_arm(rbar(sl), rx_l);
+        ++nl[sl];
+    };
+    auto wait_var = [&](int sl) {
+        mbar_wait(vbar(sl), ne[sl] & 1u);
+        if (tt == 0) mbar_arm(vbar(sl), rx_e);
+        ++ne[sl];
+    };
+
+    const int r = tt;                 // H = 1: this thread's band-0 row (if r < mbq)
+    const bool own = !producer && r < mbq;
+    const int64_t npairs = (a.frames + 1) / 2;
+    for (int64_t pi = cid; pi < npairs; pi += ncl) {
+        int64_t fs[2] = {2 * pi, 2 * pi + 1};
+        const int ns = fs[1] < a.frames ? 2 : 1;    // cluster-uniform
+        float e0[2][WR];
+        uint32_t synd[2] = {0, 0};
+        if (producer) {
+            for (int sl = 0; sl < ns; ++sl) ship_l(sl);
+            for (int t = 1; t <= a.max_iter; ++t) {
+                for (int sl = 0; sl < ns; ++sl)
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) ship_e(sl, c);
+                for (int sl = 0; sl < ns; ++sl) ship_l(sl);
+            }
+        } else {
+            // ---- V-phase 0 of both slots: L = R, E = 0; band-0 check of t = 1
+#pragma unroll
+            for (int sl = 0; sl < 2; ++sl) {
+                if (sl < ns) {
+                    float lv[WR];
+                    if (own) {
+                        const int v0 = (int(q) * mbq + r) * WR;
+                        lds_row<WR>(reinterpret_cast<const char *>(a.llr + fs[sl] * int64_t(n)), uint32_t(v0) * 4u, lv);
+#pragma unroll
+                        for (int j = 0; j < WR; ++j) lv[j] = fminf(fmaxf(lv[j], -30.0f), 30.0f) * kL2E;
+                        const uint16_t *vt = vtab + size_t(r) * WR * NB;
+#pragma unroll
+                        for (int j = 0; j < WR; ++j)
+#pragma unroll
+                            for (int b = 0; b < NB; ++b) *reinterpret_cast<float *>(varr[sl] + vt[j * NB + b]) = lv[j];
+                    }
+                    chunk_done(vchunk(sl));
+                    if (own) check_row<WR, true>(lv, e0[sl]);
+                }
+            }
+            for (int t = 1; t <= a.max_iter; ++t) {
+                // ---- C-phases (a3)
+#pragma unroll
+                for (int sl = 0; sl < 2; ++sl) {
+                    if (sl < ns) {
+                        wait_row(sl);
+#pragma unroll
+                        for (int b = 0; b < NB; ++b) {
+                            if (r < mbq) {
+                                const uint16_t *rt = rtab + (size_t(b) * mbq + r) * WR;
+                                uint32_t s_[WR];
+#pragma unroll
+                                for (int j = 0; j < WR; ++j) s_[j] = rt[j];
+                                float x[WR], e[WR];
+#pragma unroll
+                                for (int j = 0; j < WR; ++j) x[j] = *reinterpret_cast<const float *>(rowr[sl] + s_[j]);
+                                check_row<WR, true>(x, e);
+#pragma unroll
+                                for (int j = 0; j < WR; ++j) *reinterpret_cast<float *>(rowr[sl] + s_[j]) = e[j];
+                            }
+                            chunk_done(cchunk(sl, b));
+                        }
+                    }
+                }
+                // ---- V-phases (a4/a5)
+                const bool last = t == a.max_iter;
+#pragma unroll
+                for (int sl = 0; sl < 2; ++sl) {
+                    if (sl < ns) {
+                        float lv[WR];
+                        if (own)
+                            lds_row<WR>(reinterpret_cast<const char *>(a.llr + fs[sl] * int64_t(n)),
+                                        uint32_t((int(q) * mbq + r) * WR) * 4u, lv);
+                        wait_var(sl);
+                        if (own) {
+                            const uint16_t *vt = vtab + size_t(r) * WR * NB;
+                            uint32_t s_[WR * NB];
+#pragma unroll
+                            for (int i = 0; i < WR * NB; ++i) s_[i] = vt[i];
+                            float eb[WR * NB];
+#pragma unroll
+                            for (int j = 0; j < WR; ++j) {
+                                lv[j] = fminf(fmaxf(lv[j], -30.0f), 30.0f) * kL2E + e0[sl][j];
+#pragma unroll
+                                for (int b = 0; b < NB; ++b) {
+                                    eb[j * NB + b] = *reinterpret_cast<const float *>(varr[sl] + s_[j * NB + b]);
+                                    lv[j] += eb[j * NB + b];
+                                }
+                            }
+                            if (last) {
+                                uint32_t rp = 0;
+#pragma unroll
+                                for (int j = 0; j < WR; ++j) {
+                                    rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
+#pragma unroll
+                                    for (int b = 0; b < NB; ++b) *reinterpret_cast<float *>(varr[sl] + s_[j * NB + b]) = lv[j];
+                                }
+                                synd[sl] |= rp;
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < WR; ++j) {
+#pragma unroll
+                                    for (int b = 0; b < NB; ++b)
+                                        *reinterpret_cast<float *>(varr[sl] + s_[j * NB + b]) = lv[j] - eb[j * NB + b];
+                                    lv[j] -= e0[sl][j];
+                                }
+                            }
+                        }
+                        chunk_done(vchunk(sl));
+                        if (own && !last) check_row<WR, true>(lv, e0[sl]);
+                    }
+                }
+            }
+            // ---- a7: syndrome (ROW slots hold L of bands >= 1)
+#pragma unroll
+            for (int sl = 0; sl < 2; ++sl) {
+                if (sl < ns) {
+                    wait_row(sl);
+                    for (int rr = tt; rr < NB * mbq; rr += TW) {
+                        const uint16_t *rt = rtab + size_t(rr) * WR;
+                        uint32_t rp = 0;
+#pragma unroll
+                        for (int j = 0; j < WR; ++j) rp ^= (*reinterpret_cast<const float *>(rowr[sl] + rt[j]) >= 0.0f) ? 1u : 0u;
+                        synd[sl] |= rp;
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int sl = 0; sl < 2; ++sl) {
+            const int any = __syncthreads_or(synd[sl] != 0);
+            if (tt == 0) {
+                int *f0 = cg::this_cluster().map_shared_rank(flags, 0);
+                f0[sl * C + int(q)] = any;
+            }
+        }
+        cluster_sync_all();
+        if (!producer) {
+            const int nw = code.nw;
+            const int w_lo = (int(q) * nq + 31) / 32;
+            const int w_hi = (int(q) == C - 1) ? nw : ((int(q) + 1) * nq + 31) / 32;
+            const int qn = (int(q) + 1 < C) ? int(q) + 1 : int(q);
+            const uint16_t *tnext = cg::this_cluster().map_shared_rank(vtab, qn);
+            for (int sl = 0; sl < ns; ++sl) {
+                const char *vnext = cg::this_cluster().map_shared_rank(varr[sl], qn);
+                uint32_t *bits = a.bits + fs[sl] * int64_t(nw);
+                for (int base = w_lo * 32; base < w_hi * 32; base += TW) {
+                    const int v = base + tt;
+                    if (v >= w_hi * 32) break;
+                    bool z = false;
+                    if (v < n) {
+                        const int i = v - int(q) * nq;
+                        const float lv = i < nq ? *reinterpret_cast<const float *>(varr[sl] + vtab[size_t(i) * NB])
+                                                : *reinterpret_cast<const float *>(vnext + tnext[size_t(i - nq) * NB]);
+                        z = lv >= 0.0f;
+                    }
+                    const uint32_t word = __ballot_sync(0xffffffffu, z);
+                    if (lane == 0) bits[v >> 5] = word;
+                }
+                if (a.posterior) {
+                    float *dst = a.posterior + fs[sl] * int64_t(n) + int64_t(q) * nq;
+                    for (int i = tt; i < nq; i += TW)
+                        dst[i] = *reinterpret_cast<const float *>(varr[sl] + vtab[size_t(i) * NB]) * kLn2;
+                }
+                if (q == 0 && tt == 0) {
+                    int ok = 1;
+                    for (int i = 0; i < C; ++i) ok &= (flags[sl * C + i] == 0);
+                    a.syn_ok[fs[sl]] = uint8_t(ok);
+                    a.iters[fs[sl]] = a.max_iter;
+                }
+            }
+        }
+        cluster_sync_all();
+    }
+}
+
 template <int WR, int H, int MAXT>
 void *pick_x_c(int C) {
     switch (C) {
@@ -453,6 +736,31 @@ bool xcluster_plan(const ldpc_code &c, int64_t frames, bool et, XClusterPlan &p)
     const int mbq = c.n / c.wr / C;
     const int H = xband_rows_per_thread(mbq);
     p.threads = xband_threads(mbq) + 32;          // compute warps + the producer warp
+    // two frames in flight per cluster (xband2_kernel) when the view allows it
+    // and the batch has at least two frames per co-resident cluster's worth
+    if (c.dev.xslots == 2 && H == 1 && frames >= 2 && c.wr == 6 && c.wc == 3 && p.threads <= 768 &&
+        !std::getenv("LDPC_XBAND_1SLOT")) {
+        void *k2 = nullptr;
+        if (C == 16) k2 = (c.n == 64800 && !std::getenv("LDPC_NO_NFIX"))
+                              ? reinterpret_cast<void *>(&xband2_kernel<6, 3, 16, 768, 64800>)
+                              : reinterpret_cast<void *>(&xband2_kernel<6, 3, 16, 768>);
+        if (k2) {
+            const size_t smem2 = xband2_smem_bytes(c.n, c.wc, c.wr, C, c.dev.xcap);
+            if (ensure_smem_attribute(k2, smem2, C > 8)) {
+                int ncl = occupancy_clusters(k2, p.threads, smem2, C);
+                if (ncl >= 1) {
+                    p.kernel = k2;
+                    p.cluster = C;
+                    p.smem = smem2;
+                    p.capacity = 2 * int64_t(ncl);
+                    ncl = int(std::min<int64_t>(ncl, (frames + 1) / 2));
+                    p.grid = ncl * C;
+                    p.ws_bytes = 0;
+                    return true;
+                }
+            }
+        }
+    }
     void *k = nullptr;
     // compile-time n for C5 (n = 64800, C = 8, 736 threads)
     if (c.n == 64800 && c.wr == 6 && c.wc == 3 && C == 8 && H == 2 && p.threads <= 768 && !std::getenv("LDPC_NO_NFIX"))
