@@ -192,7 +192,7 @@ DeviceLayout compute_layout(const ldpc_code &c, bool with_G) {
         if (const int C = xband_cluster_size(c.n, c.wc, c.wr)) {
             L.xband_ridx = off; off = align256(off + sizeof(uint16_t) * nb);
             L.xband_sidx = off; off = align256(off + sizeof(uint16_t) * nb);
-            const size_t H = size_t(xband_rows_per_thread(c.n / c.wr / C));
+            const size_t H = size_t(xband_rows_host(c.n / c.wr / C));
             L.xband_seg = off;  off = align256(off + sizeof(int32_t) * 3 * size_t(C) * size_t(C) * H * H * size_t(c.wc - 1));
         }
     }
@@ -383,7 +383,7 @@ void bank_balance_rows(int32_t n, int32_t wc, int32_t wr, std::vector<int32_t> &
 int32_t xband_tables(const ldpc_code &c, int C, std::vector<uint16_t> &ridx, std::vector<uint16_t> &sidx,
                      std::vector<int32_t> &seg) {
     const int32_t n = c.n, wc = c.wc, wr = c.wr, NB = wc - 1, mbq = n / wr / C, nq = mbq * wr;
-    const int32_t T = xband_threads(mbq), H = xband_rows_per_thread(mbq), NC = NB * H;
+    const int32_t T = xband_threads_host(mbq), H = xband_rows_host(mbq), NC = NB * H;
     const size_t nb = size_t(NB) * size_t(n), nkey = size_t(C) * C * H * NC;
     auto key = [&](int32_t s, int32_t d, int32_t h, int32_t ch) { return ((size_t(s) * C + d) * H + h) * NC + ch; };
     std::vector<int32_t> cnt(nkey, 0), rank(nb), kof(nb);

@@ -3,6 +3,7 @@
 // oracle never includes it.
 #pragma once
 
+#include <algorithm>
 #include <cstddef>
 #include <cstdlib>
 #include <cstdint>
@@ -98,6 +99,17 @@ constexpr int xband_threads(int32_t mbq) {
     const int b0 = xband_rows_per_thread(mbq);
     return ((mbq + b0 - 1) / b0 + 31) / 32 * 32;
 }
+// Host-side choice of rows per thread (LDPC_XBAND_H raises it: experiments;
+// the compile-time-n kernels assume the default and are skipped then).
+inline int xband_rows_host(int32_t mbq) {
+    int h = xband_rows_per_thread(mbq);
+    if (const char *e = std::getenv("LDPC_XBAND_H")) h = std::max(h, std::atoi(e));
+    return h == 3 ? 4 : h;
+}
+inline int xband_threads_host(int32_t mbq) {
+    const int b0 = xband_rows_host(mbq);
+    return ((mbq + b0 - 1) / b0 + 31) / 32 * 32;
+}
 // Region capacity (floats): (wc-1) nq edge slots plus the 16-byte padding of
 // its H x (wc-1) H x C segments -- worst case 3 floats each (shared-memory
 // sizing), expected 1.5 (cluster-size choice).  The exact capacity comes
@@ -105,14 +117,14 @@ constexpr int xband_threads(int32_t mbq) {
 // overflow the 16-bit byte slots gets no exchange view.
 inline int32_t xband_capacity_bound(int32_t n, int32_t wc, int32_t wr, int32_t C, int pad_x2 = 6) {
     const int32_t mbq = n / wr / C, nq = mbq * wr;
-    const int32_t H = xband_rows_per_thread(mbq);
+    const int32_t H = xband_rows_host(mbq);
     return ((wc - 1) * nq + (pad_x2 * H * H * (wc - 1) * C + 1) / 2 + 3) & ~3;
 }
 constexpr int32_t kXbandMaxCapacity = 16383;     // floats: byte slots < 65536
 // Shared memory of the kernel for region capacity `cap`: two regions + the
 // CTA's two 16-bit slot tables + barriers and flags.
 inline size_t xband_smem_bytes(int32_t n, int32_t wc, int32_t wr, int32_t C, int32_t cap) {
-    const size_t mbq = size_t(n / wr / C), nq = mbq * size_t(wr), H = size_t(xband_rows_per_thread(int32_t(mbq)));
+    const size_t mbq = size_t(n / wr / C), nq = mbq * size_t(wr), H = size_t(xband_rows_host(int32_t(mbq)));
     return 2 * size_t(cap) * 4 + 2 * size_t(wc - 1) * nq * 2 + 16 + 8 * (2 + H + size_t(wc - 1) * H) + 4 * size_t(C);
 }
 // Cluster size of a code's exchange view.  Frames larger than one SM: the
@@ -123,7 +135,7 @@ inline size_t xband_smem_bytes(int32_t n, int32_t wc, int32_t wr, int32_t C, int
 inline bool xband_fits(int32_t n, int32_t wc, int32_t wr, int C) {
     if ((n / wr) % C) return false;
     if (xband_capacity_bound(n, wc, wr, C, 3) > kXbandMaxCapacity) return false;
-    if (xband_threads(n / wr / C) + 32 > 1024) return false;      // + the producer warp
+    if (xband_threads_host(n / wr / C) + 32 > 1024) return false;      // + the producer warp
     return xband_smem_bytes(n, wc, wr, C, xband_capacity_bound(n, wc, wr, C)) + 1024 <= 227 * 1024;
 }
 inline bool band_frame_fits_sm(int32_t n, int32_t wc) { return size_t(wc) * size_t(n) * 4 + 1024 <= 227 * 1024; }
@@ -139,7 +151,7 @@ inline bool xband2_fits(int32_t n, int32_t wc, int32_t wr) {
     constexpr int C = 16;
     if (wc != 3 || wr != 6 || (n / wr) % C) return false;
     const int32_t mbq = n / wr / C;
-    if (xband_rows_per_thread(mbq) != 1 || xband_threads(mbq) + 32 > 768) return false;
+    if (xband_rows_host(mbq) != 1 || xband_threads_host(mbq) + 32 > 768) return false;
     return xband2_smem_bytes(n, wc, wr, C, xband_capacity_bound(n, wc, wr, C)) + 1024 <= 227 * 1024;
 }
 inline int xband_cluster_size(int32_t n, int32_t wc, int32_t wr) {

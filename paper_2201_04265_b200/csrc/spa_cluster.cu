@@ -734,8 +734,8 @@ bool xcluster_plan(const ldpc_code &c, int64_t frames, bool et, XClusterPlan &p)
     if (et || !c.gallager || !c.regular_col || !c.dev.xcluster) return false;
     const int C = c.dev.xcluster;
     const int mbq = c.n / c.wr / C;
-    const int H = xband_rows_per_thread(mbq);
-    p.threads = xband_threads(mbq) + 32;          // compute warps + the producer warp
+    const int H = xband_rows_host(mbq);
+    p.threads = xband_threads_host(mbq) + 32;     // compute warps + the producer warp
     // two frames in flight per cluster (xband2_kernel) when the view allows it
     // and the batch has at least two frames per co-resident cluster's worth
     if (c.dev.xslots == 2 && H == 1 && frames >= 2 && c.wr == 6 && c.wc == 3 && p.threads <= 768 &&
