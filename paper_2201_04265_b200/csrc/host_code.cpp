@@ -932,6 +932,7 @@ ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, vo
     D.xcluster = (code->gallager && code->wc >= 2 && xcap > 0 && xcap <= ldpc::kXbandMaxCapacity)
                      ? ldpc::xband_cluster_size(code->n, code->wc, code->wr) : 0;
     D.xcap = D.xcluster ? xcap : 0;
+    D.xrows = D.xcluster ? ldpc::xband_rows_host(code->n / code->wr / D.xcluster) : 0;
     D.xslots = (D.xcluster == 16 && ldpc::xband2_fits(code->n, code->wc, code->wr) &&
                 ldpc::xband2_smem_bytes(code->n, code->wc, code->wr, 16, D.xcap) + 1024 <= 227 * 1024) ? 2 : 1;
     D.xband_ridx = D.xcluster ? reinterpret_cast<const uint16_t *>(base + L.xband_ridx) : nullptr;

@@ -70,6 +70,7 @@ struct DeviceCode {
     const int32_t *cband_vpos;
     int32_t xcluster;              // C of the exchange cluster view (0: none)
     int32_t xslots;                // 2: the view serves the two-slot kernel (xband2_kernel)
+    int32_t xrows;                 // rows per compute thread (H) the view's tables were built for
     int32_t xcap;                  // message region capacity (floats, multiple of 4)
     const uint16_t *xband_ridx;
     const uint16_t *xband_sidx;
@@ -123,8 +124,9 @@ inline int32_t xband_capacity_bound(int32_t n, int32_t wc, int32_t wr, int32_t C
 constexpr int32_t kXbandMaxCapacity = 16383;     // floats: byte slots < 65536
 // Shared memory of the kernel for region capacity `cap`: two regions + the
 // CTA's two 16-bit slot tables + barriers and flags.
-inline size_t xband_smem_bytes(int32_t n, int32_t wc, int32_t wr, int32_t C, int32_t cap) {
-    const size_t mbq = size_t(n / wr / C), nq = mbq * size_t(wr), H = size_t(xband_rows_host(int32_t(mbq)));
+inline size_t xband_smem_bytes(int32_t n, int32_t wc, int32_t wr, int32_t C, int32_t cap, int32_t rows = 0) {
+    const size_t mbq = size_t(n / wr / C), nq = mbq * size_t(wr);
+    const size_t H = size_t(rows > 0 ? rows : xband_rows_host(int32_t(mbq)));
     return 2 * size_t(cap) * 4 + 2 * size_t(wc - 1) * nq * 2 + 16 + 8 * (2 + H + size_t(wc - 1) * H) + 4 * size_t(C);
 }
 // Cluster size of a code's exchange view.  Frames larger than one SM: the

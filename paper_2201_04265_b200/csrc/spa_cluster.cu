@@ -734,8 +734,8 @@ bool xcluster_plan(const ldpc_code &c, int64_t frames, bool et, XClusterPlan &p)
     if (et || !c.gallager || !c.regular_col || !c.dev.xcluster) return false;
     const int C = c.dev.xcluster;
     const int mbq = c.n / c.wr / C;
-    const int H = xband_rows_host(mbq);
-    p.threads = xband_threads_host(mbq) + 32;     // compute warps + the producer warp
+    const int H = c.dev.xrows;                    // as the bound tables were built
+    p.threads = ((mbq + H - 1) / H + 31) / 32 * 32 + 32;     // compute warps + the producer warp
     // two frames in flight per cluster (xband2_kernel) when the view allows it
     // and the batch has at least two frames per co-resident cluster's worth
     if (c.dev.xslots == 2 && H == 1 && frames >= 2 && c.wr == 6 && c.wc == 3 && p.threads <= 768 &&
@@ -770,7 +770,7 @@ bool xcluster_plan(const ldpc_code &c, int64_t frames, bool et, XClusterPlan &p)
     p.kernel = k;
     p.cluster = C;
     if ((p.threads - 32) * H < mbq || C * H > 32) return false;
-    p.smem = xband_smem_bytes(c.n, c.wc, c.wr, C, c.dev.xcap);
+    p.smem = xband_smem_bytes(c.n, c.wc, c.wr, C, c.dev.xcap, H);
     if (!ensure_smem_attribute(k, p.smem, C > 8)) return false;
     int nclusters = occupancy_clusters(k, p.threads, p.smem, C);
     if (nclusters < 1) return false;
