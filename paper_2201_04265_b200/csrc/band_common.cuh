@@ -118,9 +118,9 @@ __device__ __forceinline__ void check_row(const float (&x)[D], float (&e)[D]) {
     }
     psi_row<D, true, VOTE>(ax, f);
     // exclusive sums Phi_j = sum_{k != j} f_k of positive terms: never
-    // total-minus-self (inf - inf, cancellation); a pairwise tree for D = 4,
-    // 6, 12 (fewer adds, shorter chains; measured +1-2 points on C3/C4),
-    // prefix + suffix otherwise
+    // total-minus-self (inf - inf, cancellation); a pairwise tree for D = 4, 6
+    // (fewer adds, shorter chains; measured +1-2 points on C3/C4), prefix +
+    // suffix otherwise (a tree for D = 12 measured -0.6 on C3-R3/4)
     float ex[D];
     if constexpr (D == 6) {
         const float a01 = f[0] + f[1], a23 = f[2] + f[3], a45 = f[4] + f[5];
@@ -132,21 +132,6 @@ __device__ __forceinline__ void check_row(const float (&x)[D], float (&e)[D]) {
         const float a01 = f[0] + f[1], a23 = f[2] + f[3];
         ex[0] = f[1] + a23; ex[1] = f[0] + a23;
         ex[2] = f[3] + a01; ex[3] = f[2] + a01;
-    } else if constexpr (D == 12) {
-        // pairs -> quads of pairs; each element adds its partner, the other
-        // pair of its quad and the other two quads
-        float p[6], qd[3];
-#pragma unroll
-        for (int i = 0; i < 6; ++i) p[i] = f[2 * i] + f[2 * i + 1];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) qd[i] = p[2 * i] + p[2 * i + 1];
-        const float oq[3] = {qd[1] + qd[2], qd[0] + qd[2], qd[0] + qd[1]};
-#pragma unroll
-        for (int i = 0; i < 6; ++i) {
-            const float rest = oq[i / 2] + p[i ^ 1];
-            ex[2 * i] = f[2 * i + 1] + rest;
-            ex[2 * i + 1] = f[2 * i] + rest;
-        }
     } else {
         float acc = 0.0f;
 #pragma unroll
