@@ -8,6 +8,9 @@
 #ifndef BAND_FUSE0
 #define BAND_FUSE0 true
 #endif
+#ifndef BAND_TINY_FUSE0
+#define BAND_TINY_FUSE0 true
+#endif
 
 struct BandArgs {
     DeviceCode code;
@@ -53,7 +56,10 @@ template <int WR, int WC, int B0, bool ET, int MODE, int NFIX = 0, bool GEN = fa
 __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const BandArgs a) {
     // measured on B200: +1.1 points on C4 (MODE 2), +0.8..1.3 on wr = 12 codes,
     // -2..3 on check-major wr = 4 / 6 codes (C3 R1/4, R1/2)
-    constexpr bool FUSE0 = BAND_FUSE0 && (MODE == 2 || WR >= 12);
+    // one-warp frames (n compiled in, <= 32 band-0 rows): latency-bound, so the
+    // psi regime votes (branches + warp syncs on the dependency chain) are off
+    constexpr bool TINY = NFIX > 0 && NFIX / WR <= 32;
+    constexpr bool FUSE0 = BAND_FUSE0 && (MODE == 2 || WR >= 12 || (TINY && BAND_TINY_FUSE0));
     constexpr bool VM = MODE >= 1, L16 = MODE == 2;
     extern __shared__ __align__(16) char smem[];
     __shared__ long long s_frame;
@@ -134,7 +140,7 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
                 if (tt < S && r < mb) {
                     float x[WR];
                     lds_row<WR>(smem, lbase + uint32_t(r) * WR * 4u, x);
-                    check_row<WR, !ET>(x, e0[k]);
+                    check_row<WR, !ET && !TINY>(x, e0[k]);
                 }
             }
         }
@@ -154,7 +160,7 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
                         if (ET) rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
                     }
                     synd |= rp;
-                    check_row<WR, !ET>(x, e0[k]);
+                    check_row<WR, !ET && !TINY>(x, e0[k]);
                 }
             }
 #pragma unroll
@@ -191,7 +197,7 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
                         if (ET) rp ^= (lv >= 0.0f) ? 1u : 0u;
                     }
                     synd |= rp;
-                    check_row<WR, !ET>(x, e);
+                    check_row<WR, !ET && !TINY>(x, e);
                     if (VM) {
 #pragma unroll
                         for (int j = 0; j < WR; ++j) *reinterpret_cast<float *>(smem + li[j] + delta) = e[j];
@@ -269,7 +275,7 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
                             float x[WR];
 #pragma unroll
                             for (int j = 0; j < WR; ++j) x[j] = lv[j] - e0[k][j];
-                            check_row<WR, !ET>(x, e0[k]);
+                            check_row<WR, !ET && !TINY>(x, e0[k]);
                         }
                     }
                 }

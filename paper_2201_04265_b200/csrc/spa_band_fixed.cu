@@ -44,6 +44,7 @@ void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode) {
         return et_pair<6, 3, 3, 2, 16200>(et);
     }
     if (wc == 3 && wr == 6 && n == 1008 && b0 == 1 && mode == 0) return et_pair<6, 3, 1, 0, 1008>(et);
+    if (wc == 3 && wr == 6 && n == 96 && b0 == 1 && mode == 0) return et_pair<6, 3, 1, 0, 96>(et);     // C1
     if (wc == 3 && n == 3996 && b0 == 1 && mode == 0) {
         if (wr == 6) return et_pair<6, 3, 1, 0, 3996>(et);
         if (wr == 12) return et_pair<12, 3, 1, 0, 3996>(et);
