@@ -8,9 +8,6 @@
 #ifndef BAND_FUSE0
 #define BAND_FUSE0 true
 #endif
-#ifndef BAND_TINY_FUSE0
-#define BAND_TINY_FUSE0 true
-#endif
 
 struct BandArgs {
     DeviceCode code;
@@ -52,14 +49,15 @@ __device__ __forceinline__ bool cta_sync_or(bool p) { return __syncthreads_or(p 
 // with six atomics when the CTA runs out of frames).
 // RPRE: band-0 rows whose R is prefetched before the check->variable barrier
 // (only when R lives in global memory).
-template <int WR, int WC, int B0, bool ET, int MODE, int NFIX = 0, bool GEN = false, int RPRE = 0>
+// NOVOTE: psi regime votes off.  The votes pay only when many iterations run
+// after a frame has converged; with few iterations (C1: 20, Table I: 10) they
+// are overhead and their branches and warp syncs lengthen the dependency
+// chain (measured: C1 +35%, Table I +6..20%).  Chosen at plan time.
+template <int WR, int WC, int B0, bool ET, int MODE, int NFIX = 0, bool GEN = false, int RPRE = 0, bool NOVOTE = false>
 __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const BandArgs a) {
     // measured on B200: +1.1 points on C4 (MODE 2), +0.8..1.3 on wr = 12 codes,
     // -2..3 on check-major wr = 4 / 6 codes (C3 R1/4, R1/2)
-    // one-warp frames (n compiled in, <= 32 band-0 rows): latency-bound, so the
-    // psi regime votes (branches + warp syncs on the dependency chain) are off
-    constexpr bool TINY = NFIX > 0 && NFIX / WR <= 32;
-    constexpr bool FUSE0 = BAND_FUSE0 && (MODE == 2 || WR >= 12 || (TINY && BAND_TINY_FUSE0));
+    constexpr bool FUSE0 = BAND_FUSE0 && (MODE == 2 || WR >= 12 || NOVOTE);
     constexpr bool VM = MODE >= 1, L16 = MODE == 2;
     extern __shared__ __align__(16) char smem[];
     __shared__ long long s_frame;
@@ -140,7 +138,7 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
                 if (tt < S && r < mb) {
                     float x[WR];
                     lds_row<WR>(smem, lbase + uint32_t(r) * WR * 4u, x);
-                    check_row<WR, !ET && !TINY>(x, e0[k]);
+                    check_row<WR, !ET && !NOVOTE>(x, e0[k]);
                 }
             }
         }
@@ -160,7 +158,7 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
                         if (ET) rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
                     }
                     synd |= rp;
-                    check_row<WR, !ET && !TINY>(x, e0[k]);
+                    check_row<WR, !ET && !NOVOTE>(x, e0[k]);
                 }
             }
 #pragma unroll
@@ -197,7 +195,7 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
                         if (ET) rp ^= (lv >= 0.0f) ? 1u : 0u;
                     }
                     synd |= rp;
-                    check_row<WR, !ET && !TINY>(x, e);
+                    check_row<WR, !ET && !NOVOTE>(x, e);
                     if (VM) {
 #pragma unroll
                         for (int j = 0; j < WR; ++j) *reinterpret_cast<float *>(smem + li[j] + delta) = e[j];
@@ -275,7 +273,7 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
                             float x[WR];
 #pragma unroll
                             for (int j = 0; j < WR; ++j) x[j] = lv[j] - e0[k][j];
-                            check_row<WR, !ET && !TINY>(x, e0[k]);
+                            check_row<WR, !ET && !NOVOTE>(x, e0[k]);
                         }
                     }
                 }

@@ -229,9 +229,15 @@ struct BandPlan {
 // false when the code is not eligible (not from ldpc_make_H, unsupported
 // (wc, wr), n % 4 != 0, or the frame does not fit one SM's shared memory).
 // variant: 0 auto, 3 check-major E, 4 variable-major E.
-bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPlan &p);
+bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPlan &p, int max_iter = 50);
 // band_kernel instantiation with n compiled in (spa_band_fixed.cu), or nullptr.
-void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode);
+void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode, int max_iter);
+// Whether the band decoder runs without psi regime votes for this code and
+// iteration count (few-iteration configs with a compile-time-n kernel).
+inline bool band_novote(int n, int wr, int wc, int max_iter, bool et) {
+    if (et || max_iter > 20 || std::getenv("LDPC_VOTES") || std::getenv("LDPC_NO_NFIX")) return false;
+    return (n == 96 && wr == 6 && wc == 3) || (n == 1032 && wr == 12 && (wc == 3 || wc == 6 || wc == 9));
+}
 ldpc_status band_launch(const ldpc_code &c, const BandPlan &p, const float *llr, int64_t frames,
                         const ldpc_decode_opts &o, uint32_t *bits, uint8_t *syn, int32_t *iters, float *post,
                         void *ws, size_t ws_bytes, void *stream);

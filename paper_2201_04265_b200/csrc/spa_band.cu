@@ -328,7 +328,7 @@ ldpc_status cluster_launch(const ldpc_code &c, const ClusterPlan &p, const float
     return e == cudaSuccess ? LDPC_OK : LDPC_ERR_CUDA;
 }
 
-bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPlan &p) {
+bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPlan &p, int max_iter) {
     if (!c.gallager || !c.regular_col || (c.n & 3)) return false;
     const int mb = c.n / c.wr;
     const int sms = device_attribute(cudaDevAttrMultiProcessorCount);
@@ -346,7 +346,7 @@ bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPla
     p.vm = variant == 4 || variant == 6 || (variant == 0 && (!p.r_in_smem || c.wc > 3));
     // 16-bit offsets (variant 6, auto with VM when n <= 16383): +2% on C4
     p.mode = p.vm ? (((variant == 6 || variant == 0) && c.n <= 16383) ? 2 : 1) : 0;
-    void *k = std::getenv("LDPC_NO_NFIX") ? nullptr : pick_band_kernel_fixed(c.n, c.wr, c.wc, b0, et, p.mode);
+    void *k = std::getenv("LDPC_NO_NFIX") ? nullptr : pick_band_kernel_fixed(c.n, c.wr, c.wc, b0, et, p.mode, max_iter);
     if (!k) k = pick_band_kernel(c.wr, c.wc, b0, et, p.mode);
     if (!k) return false;
     p.smem = p.r_in_smem ? with_r : base;

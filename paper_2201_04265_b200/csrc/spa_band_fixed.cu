@@ -23,6 +23,13 @@ void *et_pair(bool et) {
     return et ? reinterpret_cast<void *>(&band_kernel<WR, WC, B0, true, MODE, N>)
               : reinterpret_cast<void *>(&band_kernel<WR, WC, B0, false, MODE, N>);
 }
+// few iterations: the no-vote instantiation (fixed-iteration mode; under early
+// termination the votes are off anyway)
+template <int WR, int WC, int B0, int MODE, int N>
+void *et_pair_nv(bool et, bool novote) {
+    if (novote && !et) return reinterpret_cast<void *>(&band_kernel<WR, WC, B0, false, MODE, N, false, 0, true>);
+    return et_pair<WR, WC, B0, MODE, N>(et);
+}
 }  // namespace
 
 // (n, wr, wc, rows per thread, mode) as band_plan resolves them in auto mode:
@@ -30,7 +37,8 @@ void *et_pair(bool et) {
 //   check-major; Table I 1032 (wc 9/6 VM+16-bit, 3 check-major).  Measured
 //   on B200 against NFIX = 0: C2 +2.6, C4 +2.9, C3-R3/4 +0.7, Table I R1/4
 //   (100k frames) +1.3 points of the SFU roofline; C3 (3,4) -0.7 (left out).
-void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode) {
+void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode, int max_iter) {
+    const bool novote = band_novote(n, wr, wc, max_iter, et);
     if (wc == 3 && wr == 6 && n == 16200 && b0 == 3 && mode == 2) {
         // R of 2 of the 3 band-0 rows prefetched before the check->variable
         // barrier (RPRE; measured on B200: 0 rows 65.8%, 1 67.2%, 2 68.2%,
@@ -44,15 +52,15 @@ void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode) {
         return et_pair<6, 3, 3, 2, 16200>(et);
     }
     if (wc == 3 && wr == 6 && n == 1008 && b0 == 1 && mode == 0) return et_pair<6, 3, 1, 0, 1008>(et);
-    if (wc == 3 && wr == 6 && n == 96 && b0 == 1 && mode == 0) return et_pair<6, 3, 1, 0, 96>(et);     // C1
+    if (wc == 3 && wr == 6 && n == 96 && b0 == 1 && mode == 0) return et_pair_nv<6, 3, 1, 0, 96>(et, novote);   // C1
     if (wc == 3 && n == 3996 && b0 == 1 && mode == 0) {
         if (wr == 6) return et_pair<6, 3, 1, 0, 3996>(et);
         if (wr == 12) return et_pair<12, 3, 1, 0, 3996>(et);
     }
     if (wr == 12 && n == 1032 && b0 == 1) {
-        if (wc == 9 && mode == 2) return et_pair<12, 9, 1, 2, 1032>(et);
-        if (wc == 6 && mode == 2) return et_pair<12, 6, 1, 2, 1032>(et);
-        if (wc == 3 && mode == 0) return et_pair<12, 3, 1, 0, 1032>(et);
+        if (wc == 9 && mode == 2) return et_pair_nv<12, 9, 1, 2, 1032>(et, novote);
+        if (wc == 6 && mode == 2) return et_pair_nv<12, 6, 1, 2, 1032>(et, novote);
+        if (wc == 3 && mode == 0) return et_pair_nv<12, 3, 1, 0, 1032>(et, novote);
     }
     return nullptr;
 }

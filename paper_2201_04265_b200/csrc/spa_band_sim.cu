@@ -23,8 +23,14 @@ void *gen_pair(bool et) {
     return et ? reinterpret_cast<void *>(&band_kernel<6, 3, B0, true, MODE, 0, true>)
               : reinterpret_cast<void *>(&band_kernel<6, 3, B0, false, MODE, 0, true>);
 }
-void *pick_gen_kernel(int n, int wr, int wc, int b0, bool et, int mode) {
+// the same arithmetic as the ldpc_decode kernel it stands in for
+void *pick_gen_kernel(int n, int wr, int wc, int b0, bool et, int mode, int max_iter) {
     if (wr != 6 || wc != 3 || (mode != 0 && mode != 2)) return nullptr;
+    if (band_novote(n, wr, wc, max_iter, et)) {
+        if (n == 96 && b0 == 1 && mode == 0)
+            return reinterpret_cast<void *>(&band_kernel<6, 3, 1, false, 0, 96, true, 0, true>);
+        return nullptr;
+    }
     if (n == 16200 && b0 == 3 && mode == 2)         // C4, n compiled in as in ldpc_decode
         return et ? reinterpret_cast<void *>(&band_kernel<6, 3, 3, true, 2, 16200, true>)
                   : reinterpret_cast<void *>(&band_kernel<6, 3, 3, false, 2, 16200, true>);
@@ -51,9 +57,9 @@ extern "C" ldpc_status ldpc_decode_simulate(const ldpc_code *code, uint64_t seed
     const int v = opts->variant;
     if (v != 0 && v != 3 && v != 4 && v != 6) return LDPC_ERR_UNSUPPORTED;
     ldpc::BandPlan bp;
-    if (!ldpc::band_plan(*code, frames, opts->early_term != 0, v, bp)) return LDPC_ERR_UNSUPPORTED;
+    if (!ldpc::band_plan(*code, frames, opts->early_term != 0, v, bp, opts->max_iter)) return LDPC_ERR_UNSUPPORTED;
     const int b0 = std::max(1, (code->n / code->wr + 1023) / 1024);
-    void *k = ldpc::pick_gen_kernel(code->n, code->wr, code->wc, b0, opts->early_term != 0, bp.mode);
+    void *k = ldpc::pick_gen_kernel(code->n, code->wr, code->wc, b0, opts->early_term != 0, bp.mode, opts->max_iter);
     if (!k) return LDPC_ERR_UNSUPPORTED;
     if (!ldpc::ensure_smem_attribute(k, bp.smem)) return LDPC_ERR_CUDA;
     if (!d_ws || ws_bytes < bp.ws_bytes) return LDPC_ERR_ARG;

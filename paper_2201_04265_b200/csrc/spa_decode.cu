@@ -485,7 +485,7 @@ ldpc_status resolve(const ldpc_code &c, int64_t frames, const ldpc_decode_opts &
     const bool et = o.early_term != 0;
     frames = std::max<int64_t>(frames, 1);
     const bool want_band = v == 0 || v == 3 || v == 4 || v == 6;
-    const bool band_ok = want_band && band_plan(c, frames, et, v, r.band);
+    const bool band_ok = want_band && band_plan(c, frames, et, v, r.band, o.max_iter);
     if (want_band && v != 0) {
         if (!band_ok) return LDPC_ERR_UNSUPPORTED;
         r.variant = r.band.mode == 2 ? 6 : (r.band.vm ? 4 : 3);
