@@ -181,8 +181,9 @@ ldpc_status ldpc_decode_workspace_bytes(const ldpc_code *code, int64_t frames,
  * global-state (CTA per frame, any n); 3 Gallager band kernel, check-major E;
  * 4 Gallager band kernel, variable-major E (3 and 4 need an ldpc_make_H code
  * whose frame fits one SM; LDPC_ERR_UNSUPPORTED otherwise); 5 cluster band
- * kernel (ldpc_make_H codes too large for one SM, wr = 6, fixed iterations;
- * remote messages through L2-resident global copies); 6 = 4 with 16-bit
+ * kernel (ldpc_make_H codes too large for one SM, wr = 6; remote messages
+ * through L2-resident global copies; the auto choice for such codes under
+ * early termination); 6 = 4 with 16-bit
  * offsets (n <= 16383); 7 exchange cluster kernel (same codes as 5; a
  * cluster of C CTAs per frame trades message segments with bulk DSMEM copies,
  * no workspace; fixed iterations, wr = 6).  Auto (0): a frame that fits one SM

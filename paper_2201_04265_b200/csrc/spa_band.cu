@@ -115,7 +115,12 @@ struct ClusterArgs {
     int64_t slot_floats;
 };
 
-template <int WR, int WC, int B0, int C>
+// ET: early termination (reading Q11).  The syndrome of z^{t-1} is computed in
+// check phase t from the L values the rows read anyway; each CTA ORs its rows
+// into iflags[q] before the cluster barrier that ends the check phase, and
+// every CTA reads all C flags after it, so the stop decision is uniform over
+// the cluster (the flags are rewritten only after the next barrier).
+template <int WR, int WC, int B0, int C, bool ET>
 __global__ void __launch_bounds__(1024, 1) band_cluster_kernel(const ClusterArgs a) {
     extern __shared__ __align__(16) char smem[];
     const DeviceCode &code = a.code;
@@ -132,6 +137,7 @@ __global__ void __launch_bounds__(1024, 1) band_cluster_kernel(const ClusterArgs
     float *Eg = Lg + n;
     float *Rg = Eg + int64_t(NB) * n;
     int *flags = reinterpret_cast<int *>(Rg + n);
+    int *iflags = flags + 32;                      // per-iteration syndrome flags (ET)
     const int32_t *lidx = code.cband_lidx;
     const int32_t *vpos = code.cband_vpos;
 
@@ -156,17 +162,25 @@ __global__ void __launch_bounds__(1024, 1) band_cluster_kernel(const ClusterArgs
             for (int j = 0; j < WR; ++j) e0[k][j] = 0.0f;
         cluster_sync_all();
 
+        int32_t iters = a.max_iter;
+        bool stopped = false;
         for (int t = 1; t <= a.max_iter; ++t) {
-            // check phase over own rows
+            // check phase over own rows (and the syndrome of z^{t-1} when ET)
+            uint32_t synd = 0;
 #pragma unroll
             for (int k = 0; k < B0; ++k) {
                 const int r = tt + k * T;
                 if (r < mbq) {
                     float lv[WR], x[WR];
                     lds_row<WR>(reinterpret_cast<const char *>(Ls), uint32_t(r) * WR * 4u, lv);
+                    uint32_t rp = 0;
 #pragma unroll
-                    for (int j = 0; j < WR; ++j) x[j] = lv[j] - e0[k][j];
-                    check_row<WR, true>(x, e0[k]);
+                    for (int j = 0; j < WR; ++j) {
+                        x[j] = lv[j] - e0[k][j];
+                        if (ET) rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
+                    }
+                    synd |= rp;
+                    check_row<WR, !ET>(x, e0[k]);
                 }
             }
 #pragma unroll
@@ -179,14 +193,33 @@ __global__ void __launch_bounds__(1024, 1) band_cluster_kernel(const ClusterArgs
                     float e[WR], x[WR];
                     ldg_idx<WR>(lidx + gpos, li);
                     lds_row<WR>(smem, uint32_t(r) * WR * 4u, e);
+                    uint32_t rp = 0;
 #pragma unroll
-                    for (int j = 0; j < WR; ++j) x[j] = ld_l_or_g(smem, Lg, li[j]) - e[j];
-                    check_row<WR, true>(x, e);
+                    for (int j = 0; j < WR; ++j) {
+                        const float lv = ld_l_or_g(smem, Lg, li[j]);
+                        x[j] = lv - e[j];
+                        if (ET) rp ^= (lv >= 0.0f) ? 1u : 0u;
+                    }
+                    synd |= rp;
+                    check_row<WR, !ET>(x, e);
                     sts_row<WR>(smem, uint32_t(r) * WR * 4u, e);
                     sts_row<WR>(reinterpret_cast<char *>(Eg + gpos), 0u, e);
                 }
             }
+            if (ET) {
+                const int any = __syncthreads_or(synd != 0);
+                if (tt == 0) iflags[q] = any;
+            }
             cluster_sync_all();
+            if (ET && t > 1) {
+                int any = 0;
+                for (int i = 0; i < C; ++i) any |= __ldcg(iflags + i);
+                if (!any) {                        // z^{t-1} has zero syndrome: stop (reading c6)
+                    iters = t - 1;
+                    stopped = true;
+                    break;
+                }
+            }
             // variable phase over own variables
 #pragma unroll
             for (int k = 0; k < B0; ++k) {
@@ -244,29 +277,29 @@ __global__ void __launch_bounds__(1024, 1) band_cluster_kernel(const ClusterArgs
         if (q == 0 && tt == 0) {
             int ok = 1;
             for (int i = 0; i < C; ++i) ok &= (__ldcg(flags + i) == 0);
-            a.syn_ok[f] = uint8_t(ok);
-            a.iters[f] = a.max_iter;
+            a.syn_ok[f] = uint8_t(ok || stopped);
+            a.iters[f] = iters;
         }
         cluster_sync_all();     // Lg / flags are reused by the next frame
     }
 }
 
-template <int WR, int B0>
+template <int WR, int B0, bool ET>
 void *pick_cluster_c(int C) {
     switch (C) {
-        case 2: return reinterpret_cast<void *>(&band_cluster_kernel<WR, 3, B0, 2>);
-        case 4: return reinterpret_cast<void *>(&band_cluster_kernel<WR, 3, B0, 4>);
-        case 8: return reinterpret_cast<void *>(&band_cluster_kernel<WR, 3, B0, 8>);
+        case 2: return reinterpret_cast<void *>(&band_cluster_kernel<WR, 3, B0, 2, ET>);
+        case 4: return reinterpret_cast<void *>(&band_cluster_kernel<WR, 3, B0, 4, ET>);
+        case 8: return reinterpret_cast<void *>(&band_cluster_kernel<WR, 3, B0, 8, ET>);
     }
     return nullptr;
 }
 
-void *pick_cluster_kernel(int wr, int wc, int b0, int C) {
+void *pick_cluster_kernel(int wr, int wc, int b0, int C, bool et) {
     if (wc != 3 || wr != 6) return nullptr;
     switch (b0) {
-        case 1: return pick_cluster_c<6, 1>(C);
-        case 2: return pick_cluster_c<6, 2>(C);
-        case 3: return pick_cluster_c<6, 3>(C);
+        case 1: return et ? pick_cluster_c<6, 1, true>(C) : pick_cluster_c<6, 1, false>(C);
+        case 2: return et ? pick_cluster_c<6, 2, true>(C) : pick_cluster_c<6, 2, false>(C);
+        case 3: return et ? pick_cluster_c<6, 3, true>(C) : pick_cluster_c<6, 3, false>(C);
     }
     return nullptr;
 }
@@ -274,13 +307,13 @@ void *pick_cluster_kernel(int wr, int wc, int b0, int C) {
 }  // namespace
 
 bool cluster_plan(const ldpc_code &c, int64_t frames, bool et, ClusterPlan &p) {
-    if (et || !c.gallager || !c.regular_col || (c.n & 3)) return false;
+    if (!c.gallager || !c.regular_col || (c.n & 3)) return false;
     const int C = band_cluster_size(c.n, c.wc, c.wr);
     if (C == 0) return false;
     const int mbq = c.n / c.wr / C, nq = c.n / C;
     if (nq & 3) return false;
     const int b0 = std::max(1, (mbq + 1023) / 1024);
-    void *k = pick_cluster_kernel(c.wr, c.wc, b0, C);
+    void *k = pick_cluster_kernel(c.wr, c.wc, b0, C, et);
     if (!k) return false;
     p.kernel = k;
     p.cluster = C;
@@ -291,7 +324,7 @@ bool cluster_plan(const ldpc_code &c, int64_t frames, bool et, ClusterPlan &p) {
     if (nclusters < 1) return false;
     nclusters = int(std::min<int64_t>(nclusters, std::max<int64_t>(frames, 1)));
     p.grid = nclusters * C;
-    p.slot_floats = (int64_t(c.wc + 1) * c.n + 16 + 63) & ~int64_t(63);
+    p.slot_floats = (int64_t(c.wc + 1) * c.n + 64 + 63) & ~int64_t(63);     // + flags[32], iflags[32]
     p.ws_bytes = size_t(nclusters) * size_t(p.slot_floats) * 4;
     return true;
 }
