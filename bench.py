@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--frames", type=int, default=0, help="override frames per GPU per step")
     ap.add_argument("--e2e-frames", type=int, default=0, help="cap on e2e frames per step (0 = the batch)")
     ap.add_argument("--e2e-chunk", type=int, default=8192, help="frames per H2D/compute/D2H pipeline chunk (e2e)")
+    ap.add_argument("--early-term", type=int, choices=[0, 1], default=None,
+                    help="override the config's early termination (measurement variant)")
+    ap.add_argument("--ebn0", type=float, default=None, help="override the config's Eb/N0 in dB (measurement variant)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--eager", action="store_true", help="launch the step's kernels eagerly instead of replaying a CUDA graph")
@@ -70,7 +73,7 @@ def run_stream(args):
 
     import paper_2201_04265_b200 as L
     torch.cuda.set_device(0)
-    wl = W.ALL[args.config]
+    wl = workload(args)
     code = L.ldpc_code_bind_device(L.ldpc_make_G(L.ldpc_make_H(wl.n, wl.wc, wl.wr, W.CODE_SEED)))
     k, n = code.info.k, code.info.n
     G = 64
@@ -131,7 +134,7 @@ def run_simulate(args):
 
     import paper_2201_04265_b200 as L
     torch.cuda.set_device(0)
-    wl = W.ALL[args.config]
+    wl = workload(args)
     F = args.frames or min(wl.frames, 32768)
     code = L.ldpc_code_bind_device(L.ldpc_make_G(L.ldpc_make_H(wl.n, wl.wc, wl.wr, W.CODE_SEED)))
     k, n = code.info.k, code.info.n
@@ -190,6 +193,18 @@ def run_simulate(args):
                       "note": "each step: gen_info + encode + (channel + decode + count | fused simulate) on new frames; "
                               "counters of the two arms identical"}), flush=True)
     return 0
+
+
+def workload(args):
+    """BASELINE.json workload named by --config, with the --early-term /
+    --ebn0 overrides (measurement variants; the config's own values by default)."""
+    import dataclasses
+    wl = W.ALL[args.config]
+    if args.early_term is not None:
+        wl = dataclasses.replace(wl, early_term=bool(args.early_term))
+    if args.ebn0 is not None:
+        wl = dataclasses.replace(wl, ebn0_db=(float(args.ebn0),))
+    return wl
 
 
 def measured_peaks():
@@ -279,7 +294,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    wl = W.ALL[args.config]
+    wl = workload(args)
     threads = max(1, min(os.cpu_count() or 1, 128))
     per_thread = 1
     # warm-up / timed steps, each a bounded sample (one frame per host thread)
@@ -355,7 +370,7 @@ def main():
     if launched:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", torch.cuda.current_device())
-    wl = W.ALL[args.config]
+    wl = workload(args)
     frames = args.frames or (wl.frames if wl.frames * wl.n * 4 < 40e9 else 16384)
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
