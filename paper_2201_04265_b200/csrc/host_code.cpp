@@ -416,6 +416,76 @@ int32_t xband_tables(const ldpc_code &c, int C, std::vector<uint16_t> &ridx, std
     }
     for (size_t i = 0; i < nkey; ++i) bytes[i] = 4 * pad(cnt[i]);
     if (cap > kXbandMaxCapacity) return cap;     // 16-bit byte slots overflow: the caller drops the view
+    // V-phase bank balancing through the ranks: an edge's rank inside its
+    // segment fixes its VAR-region bank ((varOff + r) mod 32) and its ROW
+    // slot.  A V-phase warp instruction gathers (variable j, band b) of the 32
+    // band-0 rows of one warp window, so ranks are dealt greedily to give each
+    // such instruction distinct banks (the C-phase is balanced afterwards by
+    // reordering rows and elements, which keeps the ranks).
+    if (!std::getenv("LDPC_NO_BANKOPT")) {
+        std::vector<std::vector<int32_t>> avail(nkey * 32);
+        for (size_t k = 0; k < nkey; ++k)
+            for (int32_t r = cnt[k] - 1; r >= 0; --r) avail[k * 32 + size_t((varOff[k] / 4 + r) & 31)].push_back(r);
+        const int32_t nwin = (T + 31) / 32;
+        const size_t ninstr = size_t(C) * H * nwin * wr * NB;
+        std::vector<std::vector<int32_t>> instr(ninstr);
+        for (int32_t b = 0; b < NB; ++b)
+            for (int32_t p = 0; p < n; ++p) {
+                const int32_t v = c.col_idx[size_t(b + 1) * n + p];
+                const int32_t s = v / nq, vl = v - s * nq, rl = vl / wr, j = vl - rl * wr;
+                const int32_t h = rl / T, w = (rl % T) / 32;
+                instr[((size_t(s) * H + h) * nwin + w) * size_t(wr * NB) + size_t(j * NB + b)].push_back(b * n + p);
+            }
+        double before = 0, after = 0;
+        int ninst = 0;
+        for (auto &ins : instr) {
+            if (ins.empty()) continue;
+            if (std::getenv("LDPC_DEBUG")) {
+                int hcount[32] = {0}, mx = 0;
+                for (int32_t e : ins) mx = std::max(mx, ++hcount[(varOff[size_t(kof[size_t(e)])] / 4 + rank[size_t(e)]) & 31]);
+                before += mx;
+            }
+            // edges with the fewest usable banks first
+            std::vector<std::pair<int, int32_t>> order;
+            for (int32_t e : ins) {
+                const size_t k = size_t(kof[size_t(e)]);
+                int opts = 0;
+                for (int m = 0; m < 32; ++m) opts += !avail[k * 32 + size_t(m)].empty();
+                order.push_back({opts, e});
+            }
+            std::sort(order.begin(), order.end());
+            uint32_t used = 0;
+            int hcount[32] = {0};
+            for (const auto &oe : order) {
+                const int32_t e = oe.second;
+                const size_t k = size_t(kof[size_t(e)]);
+                int best = -1;
+                size_t bs = 0;
+                for (int m = 0; m < 32; ++m) {
+                    const size_t sz = avail[k * 32 + size_t(m)].size();
+                    if (sz && !(used >> m & 1u) && sz > bs) { bs = sz; best = m; }
+                }
+                if (best < 0)
+                    for (int m = 0; m < 32; ++m) {
+                        const size_t sz = avail[k * 32 + size_t(m)].size();
+                        if (sz > bs) { bs = sz; best = m; }
+                    }
+                rank[size_t(e)] = avail[k * 32 + size_t(best)].back();
+                avail[k * 32 + size_t(best)].pop_back();
+                used |= 1u << best;
+                hcount[best]++;
+            }
+            if (std::getenv("LDPC_DEBUG")) {
+                int mx = 0;
+                for (int m = 0; m < 32; ++m) mx = std::max(mx, hcount[m]);
+                after += mx;
+                ++ninst;
+            }
+        }
+        if (std::getenv("LDPC_DEBUG") && ninst)
+            std::fprintf(stderr, "ldpc xband bank_balance: V-phase %.3f -> %.3f wavefronts per gather\n", before / ninst,
+                         after / ninst);
+    }
     ridx.assign(nb, 0);
     sidx.assign(nb, 0);
     for (int32_t b = 0; b < NB; ++b)
