@@ -223,6 +223,184 @@ DeviceLayout compute_layout(const ldpc_code &c, bool with_G) {
 // (band, position, element) (the byte offset of L_v relative to L; a
 // band-constant shift does not change conflicts); only its order changes.
 // Deterministic.
+// Proper edge colouring of a bipartite multigraph with K colours (Koenig:
+// possible when every node has degree <= K).  Edges e = (eu[e], ev[e]) are
+// coloured one by one; when no colour is free at both ends, the path from
+// the v end alternating colours a (free at u) and b (free at v) is flipped --
+// it cannot reach u (bipartite) -- which frees a at v.  ecol[e] in [0, K).
+static void koenig_colour(const std::vector<int32_t> &eu, const std::vector<int32_t> &ev, int32_t nu, int32_t nv,
+                          int32_t K, std::vector<int32_t> &ecol) {
+    const size_t ne = eu.size();
+    ecol.assign(ne, -1);
+    std::vector<int32_t> at_u(size_t(nu) * K, -1), at_v(size_t(nv) * K, -1), path;
+    for (size_t e = 0; e < ne; ++e) {
+        const int32_t u = eu[e], v = ev[e];
+        int32_t a = -1, b = -1, c = -1;
+        for (int32_t k = 0; k < K; ++k) {
+            const bool fu = at_u[size_t(u) * K + k] < 0, fv = at_v[size_t(v) * K + k] < 0;
+            if (fu && fv) { c = k; break; }
+            if (fu && a < 0) a = k;
+            if (fv && b < 0) b = k;
+        }
+        if (c < 0) {
+            path.clear();
+            int32_t node = v, cc = a;
+            bool at_v_side = true;
+            for (;;) {
+                const int32_t ed = at_v_side ? at_v[size_t(node) * K + cc] : at_u[size_t(node) * K + cc];
+                if (ed < 0) break;
+                path.push_back(ed);
+                node = at_v_side ? eu[size_t(ed)] : ev[size_t(ed)];
+                at_v_side = !at_v_side;
+                cc = cc == a ? b : a;
+            }
+            for (int32_t ed : path) {
+                at_u[size_t(eu[size_t(ed)]) * K + ecol[size_t(ed)]] = -1;
+                at_v[size_t(ev[size_t(ed)]) * K + ecol[size_t(ed)]] = -1;
+            }
+            for (int32_t ed : path) {
+                ecol[size_t(ed)] = ecol[size_t(ed)] == a ? b : a;
+                at_u[size_t(eu[size_t(ed)]) * K + ecol[size_t(ed)]] = ed;
+                at_v[size_t(ev[size_t(ed)]) * K + ecol[size_t(ed)]] = ed;
+            }
+            c = a;
+        }
+        ecol[e] = c;
+        at_u[size_t(u) * K + c] = int32_t(e);
+        at_v[size_t(v) * K + c] = int32_t(e);
+    }
+}
+
+// Element columns of one window: wb[i*wr + j] = bank of row i's j-th element
+// (nr rows); col[i*wr + j] = the column it is stored in.  A column's cost is
+// its largest bank multiplicity.  With c_q the window's count of bank q and
+// g = max(0, max_q c_q - wr): g "double" columns take each bank at most
+// twice, the other wr - g at most once, so the window costs wr + g
+// wavefronts over its wr gathers (the least a histogram with a bank seen
+// wr + g times allows when every bank fits in two double columns).  Which of
+// a row's elements go to the double columns is a bipartite flow: row i sends
+// exactly g, bank q receives between c_q - (wr - g) and 2g; then the single
+// part (degrees <= wr - g) and the double part (banks split in two nodes of
+// degree <= g) are each Koenig-coloured.  If that flow does not exist, g is
+// raised; past wr, every bank is split in nodes of <= wr edges and coloured
+// with wr colours (a bank seen c times lands <= ceil(c / wr) times a column).
+static void color_window_elements(const std::vector<int32_t> &wb, int32_t nr, int32_t wr, std::vector<int32_t> &col) {
+    col.assign(size_t(nr) * wr, 0);
+    int32_t cnt[32] = {0};
+    for (int32_t i = 0; i < nr * wr; ++i) cnt[wb[size_t(i)]]++;
+    const int32_t cmax = *std::max_element(cnt, cnt + 32);
+    std::vector<int32_t> eu, ev, ecol, mult(size_t(nr) * 32), flow(size_t(nr) * 32), prev(nr + 32 + 2);
+    bool done = false;
+    for (int32_t g = std::max(0, cmax - wr); g < wr && !done; ++g) {
+        bool ok = true;
+        std::vector<uint8_t> dbl(size_t(nr) * wr, 0);
+        if (g > 0) {
+            std::fill(mult.begin(), mult.end(), 0);
+            std::fill(flow.begin(), flow.end(), 0);
+            for (int32_t i = 0; i < nr; ++i)
+                for (int32_t j = 0; j < wr; ++j) mult[size_t(i) * 32 + wb[size_t(i) * wr + j]]++;
+            std::vector<int32_t> rowf(nr, 0), bankf(32, 0), lo(32), hi(32);
+            for (int q = 0; q < 32; ++q) lo[q] = std::max(0, cnt[q] - (wr - g));
+            // BFS augmenting paths s -> row -> bank (forward if flow < mult,
+            // backward if flow > 0) -> t; bound[] caps bank -> t
+            auto augment = [&](const std::vector<int32_t> &bound) {
+                for (;;) {
+                    // nodes: rows 0..nr-1, banks nr..nr+31
+                    std::fill(prev.begin(), prev.end(), -2);
+                    std::vector<int32_t> qu;
+                    for (int32_t i = 0; i < nr; ++i)
+                        if (rowf[size_t(i)] < g) { prev[size_t(i)] = -1; qu.push_back(i); }
+                    int32_t hit = -1;
+                    for (size_t h = 0; h < qu.size() && hit < 0; ++h) {
+                        const int32_t x = qu[h];
+                        if (x < nr) {
+                            for (int q = 0; q < 32; ++q)
+                                if (prev[size_t(nr + q)] == -2 && flow[size_t(x) * 32 + q] < mult[size_t(x) * 32 + q]) {
+                                    prev[size_t(nr + q)] = x;
+                                    if (bankf[q] < bound[q]) { hit = nr + q; break; }
+                                    qu.push_back(nr + q);
+                                }
+                        } else {
+                            const int q = x - nr;
+                            for (int32_t i = 0; i < nr; ++i)
+                                if (prev[size_t(i)] == -2 && flow[size_t(i) * 32 + q] > 0) {
+                                    prev[size_t(i)] = x;
+                                    qu.push_back(i);
+                                }
+                        }
+                    }
+                    if (hit < 0) return;
+                    bankf[hit - nr]++;
+                    int32_t x = hit;
+                    while (prev[size_t(x)] != -1) {
+                        const int32_t y = prev[size_t(x)];
+                        if (x >= nr) flow[size_t(y) * 32 + (x - nr)]++;      // row y -> bank x
+                        else flow[size_t(x) * 32 + (y - nr)]--;              // bank y -> row x (undo)
+                        x = y;
+                    }
+                    rowf[size_t(x)]++;
+                }
+            };
+            augment(lo);
+            for (int q = 0; q < 32; ++q) ok = ok && bankf[q] >= lo[q];
+            if (ok) {
+                for (int q = 0; q < 32; ++q) hi[q] = 2 * g;
+                augment(hi);
+                for (int32_t i = 0; i < nr; ++i) ok = ok && rowf[size_t(i)] == g;
+            }
+            if (!ok) continue;
+            for (int32_t i = 0; i < nr; ++i) {
+                int32_t take[32];
+                for (int q = 0; q < 32; ++q) take[q] = flow[size_t(i) * 32 + q];
+                for (int32_t j = 0; j < wr; ++j)
+                    if (take[wb[size_t(i) * wr + j]] > 0) { take[wb[size_t(i) * wr + j]]--; dbl[size_t(i) * wr + j] = 1; }
+            }
+        }
+        // single part: colours [0, wr - g)
+        eu.clear(); ev.clear();
+        std::vector<size_t> idx;
+        for (int32_t i = 0; i < nr * wr; ++i)
+            if (!dbl[size_t(i)]) { eu.push_back(i / wr); ev.push_back(wb[size_t(i)]); idx.push_back(size_t(i)); }
+        koenig_colour(eu, ev, nr, 32, wr - g, ecol);
+        for (size_t e = 0; e < idx.size(); ++e) col[idx[e]] = ecol[e];
+        if (g > 0) {
+            eu.clear(); ev.clear(); idx.clear();
+            int32_t seen[32] = {0};
+            for (int32_t i = 0; i < nr * wr; ++i)
+                if (dbl[size_t(i)]) {
+                    const int32_t q = wb[size_t(i)];
+                    eu.push_back(i / wr);
+                    ev.push_back(q * 2 + seen[q]++ / g);
+                    idx.push_back(size_t(i));
+                }
+            koenig_colour(eu, ev, nr, 64, g, ecol);
+            for (size_t e = 0; e < idx.size(); ++e) col[idx[e]] = wr - g + ecol[e];
+        }
+        done = true;
+    }
+    if (!done) {
+        // fallback: banks split in nodes of <= wr edges, wr colours
+        int32_t seen[32] = {0};
+        const int32_t maxk = (cmax + wr - 1) / wr;
+        eu.clear(); ev.clear();
+        for (int32_t i = 0; i < nr * wr; ++i) {
+            const int32_t q = wb[size_t(i)];
+            eu.push_back(i / wr);
+            ev.push_back(q * maxk + seen[q]++ / wr);
+        }
+        koenig_colour(eu, ev, nr, 32 * maxk, wr, ecol);
+        for (int32_t i = 0; i < nr * wr; ++i) col[size_t(i)] = ecol[size_t(i)];
+    }
+    // every row's columns must be a permutation of 0..wr-1 (they are by
+    // construction; a row that is not keeps its order)
+    for (int32_t i = 0; i < nr; ++i) {
+        uint64_t m = 0;
+        for (int32_t j = 0; j < wr; ++j) m |= uint64_t(1) << col[size_t(i) * wr + j];
+        if (m != (wr == 64 ? ~uint64_t(0) : (uint64_t(1) << wr) - 1))
+            for (int32_t j = 0; j < wr; ++j) col[size_t(i) * wr + j] = j;
+    }
+}
+
 // Core of the balancing: rows[0 .. nrows*wr) (byte offsets; bank = offset/4
 // mod 32) are partitioned into the given windows (start, len) of consecutive
 // row positions.  Rows are moved between windows to flatten each window's
@@ -239,86 +417,101 @@ void balance_windows(int32_t *rowsv, int32_t nrows, int32_t wr, const std::vecto
     std::vector<int32_t> H(size_t(nw) * 32, 0);
     for (int32_t r = 0; r < nrows; ++r)
         for (int32_t j = 0; j < wr; ++j) H[size_t(row_win[size_t(r)]) * 32 + bank(rowsv[size_t(r) * wr + j])]++;
+    // cost: squared deviation from the flat histogram plus a heavy penalty on
+    // counts above the element count wr (ceil of the flat count for a short
+    // window): a bank seen at most wr times in a window can be spread over the
+    // wr element columns without a conflict (below), one seen more cannot
+    std::vector<int32_t> capw(static_cast<size_t>(nw));
+    for (int32_t w = 0; w < nw; ++w) capw[size_t(w)] = (wlen[size_t(w)] * wr + 31) / 32;
     auto cost_of = [&](int32_t w, const int32_t *h) {
         int64_t s = 0;
+        const int32_t cap = capw[size_t(w)];
         for (int q = 0; q < 32; ++q) {
             const int64_t d = int64_t(h[q]) * 32 - int64_t(wlen[size_t(w)]) * wr;
-            s += d * d;
+            const int64_t o = std::max<int64_t>(0, h[q] - cap);
+            s += d * d + o * o * 65536;
         }
         return s;
+    };
+    auto try_swap = [&](int32_t r, int32_t s, int32_t *ha, int32_t *hb, int64_t &delta) {
+        const int32_t wa = row_win[size_t(r)], wb = row_win[size_t(s)];
+        std::copy(&H[size_t(wa) * 32], &H[size_t(wa) * 32] + 32, ha);
+        std::copy(&H[size_t(wb) * 32], &H[size_t(wb) * 32] + 32, hb);
+        const int64_t c0 = cost_of(wa, ha) + cost_of(wb, hb);
+        for (int32_t j = 0; j < wr; ++j) {
+            const int br = bank(rowsv[size_t(r) * wr + j]), bs = bank(rowsv[size_t(s) * wr + j]);
+            ha[br]--; ha[bs]++; hb[bs]--; hb[br]++;
+        }
+        delta = cost_of(wa, ha) + cost_of(wb, hb) - c0;
+    };
+    auto commit_swap = [&](int32_t r, int32_t s, const int32_t *ha, const int32_t *hb) {
+        const int32_t wa = row_win[size_t(r)], wb = row_win[size_t(s)];
+        std::copy(ha, ha + 32, &H[size_t(wa) * 32]);
+        std::copy(hb, hb + 32, &H[size_t(wb) * 32]);
+        row_win[size_t(r)] = wb;
+        row_win[size_t(s)] = wa;
     };
     if (nw > 1) {
         const int64_t attempts = int64_t(nrows) * 200;
         int32_t ha[32], hb[32];
         for (int64_t t = 0; t < attempts; ++t) {
             const int32_t r = int32_t(rng.next() % uint64_t(nrows)), s = int32_t(rng.next() % uint64_t(nrows));
-            const int32_t wa = row_win[size_t(r)], wb = row_win[size_t(s)];
-            if (wa == wb) continue;
-            std::copy(&H[size_t(wa) * 32], &H[size_t(wa) * 32] + 32, ha);
-            std::copy(&H[size_t(wb) * 32], &H[size_t(wb) * 32] + 32, hb);
-            const int64_t c0 = cost_of(wa, ha) + cost_of(wb, hb);
-            for (int32_t j = 0; j < wr; ++j) {
-                const int br = bank(rowsv[size_t(r) * wr + j]), bs = bank(rowsv[size_t(s) * wr + j]);
-                ha[br]--; ha[bs]++; hb[bs]--; hb[br]++;
-            }
-            const int64_t c1 = cost_of(wa, ha) + cost_of(wb, hb);
-            if (c1 < c0) {
-                std::copy(ha, ha + 32, &H[size_t(wa) * 32]);
-                std::copy(hb, hb + 32, &H[size_t(wb) * 32]);
-                row_win[size_t(r)] = wb;
-                row_win[size_t(s)] = wa;
-            }
+            if (row_win[size_t(r)] == row_win[size_t(s)]) continue;
+            int64_t d;
+            try_swap(r, s, ha, hb, d);
+            if (d < 0) commit_swap(r, s, ha, hb);
+        }
+        // targeted passes: for every over-full (window, bank), move one of the
+        // window's rows holding that bank out, to the best of a few random
+        // partners
+        int32_t bha[32], bhb[32];
+        std::vector<std::vector<int32_t>> mem(static_cast<size_t>(nw));
+        for (int pass = 0; pass < 60; ++pass) {
+            for (auto &m : mem) m.clear();
+            for (int32_t r = 0; r < nrows; ++r) mem[size_t(row_win[size_t(r)])].push_back(r);
+            int64_t moved = 0;
+            for (int32_t w = 0; w < nw; ++w)
+                for (int q = 0; q < 32; ++q) {
+                    if (H[size_t(w) * 32 + q] <= capw[size_t(w)]) continue;
+                    int32_t cand[64], nc = 0;
+                    for (int32_t r : mem[size_t(w)]) {
+                        if (row_win[size_t(r)] != w) continue;
+                        for (int32_t j = 0; j < wr; ++j)
+                            if (bank(rowsv[size_t(r) * wr + j]) == q) { if (nc < 64) cand[nc++] = r; break; }
+                    }
+                    if (!nc) continue;
+                    const int32_t r = cand[rng.next() % uint64_t(nc)];
+                    int64_t best = 0;
+                    int32_t bs = -1;
+                    for (int k = 0; k < 48; ++k) {
+                        const int32_t s = int32_t(rng.next() % uint64_t(nrows));
+                        if (row_win[size_t(s)] == w) continue;
+                        int64_t d;
+                        try_swap(r, s, ha, hb, d);
+                        if (d < best) { best = d; bs = s; std::copy(ha, ha + 32, bha); std::copy(hb, hb + 32, bhb); }
+                    }
+                    if (bs >= 0) { commit_swap(r, bs, bha, bhb); ++moved; }
+                }
+            if (!moved) break;
         }
     }
     std::vector<std::vector<int32_t>> members(static_cast<size_t>(nw));
     for (int32_t r = 0; r < nrows; ++r) members[size_t(row_win[size_t(r)])].push_back(r);
     std::vector<int32_t> out(static_cast<size_t>(nrows) * wr);
-    std::vector<int32_t> cnt(size_t(wr) * 32);
-    std::vector<int32_t> el;
+    // Element order of a window (color_window_elements): every element column
+    // of the window hits distinct banks where the window's histogram allows.
+    std::vector<int32_t> wb, col;
     for (int32_t w = 0; w < nw; ++w) {
         const auto &mem = members[size_t(w)];
-        std::fill(cnt.begin(), cnt.end(), 0);
+        const int32_t nr = int32_t(mem.size());
+        wb.resize(size_t(nr) * wr);
+        for (int32_t i = 0; i < nr; ++i)
+            for (int32_t j = 0; j < wr; ++j) wb[size_t(i) * wr + j] = bank(rowsv[size_t(mem[size_t(i)]) * wr + j]);
+        color_window_elements(wb, nr, wr, col);
         int32_t *dst = out.data() + size_t(wstart[size_t(w)]) * wr;
-        for (size_t i = 0; i < mem.size(); ++i) {
-            el.assign(rowsv + size_t(mem[i]) * wr, rowsv + size_t(mem[i]) * wr + wr);
-            // most constrained variables first (their bank is busiest)
-            std::sort(el.begin(), el.end(), [&](int32_t x, int32_t y) {
-                int cx = 0, cy = 0;
-                for (int32_t j = 0; j < wr; ++j) { cx += cnt[size_t(j) * 32 + bank(x)]; cy += cnt[size_t(j) * 32 + bank(y)]; }
-                return cx > cy || (cx == cy && x < y);
-            });
-            uint32_t used = 0;
-            int32_t *row = dst + i * wr;
-            for (int32_t v : el) {
-                int32_t best = -1, bc = 1 << 30;
-                for (int32_t j = 0; j < wr; ++j)
-                    if (!(used >> j & 1u) && cnt[size_t(j) * 32 + bank(v)] < bc) { bc = cnt[size_t(j) * 32 + bank(v)]; best = j; }
-                used |= 1u << best;
-                row[best] = v;
-                cnt[size_t(best) * 32 + bank(v)]++;
-            }
-        }
-        // repair: swap two elements of a row when it lowers the column conflicts
-        for (int pass = 0; pass < 8; ++pass) {
-            bool any = false;
-            for (size_t i = 0; i < mem.size(); ++i) {
-                int32_t *row = dst + i * wr;
-                for (int32_t x = 0; x < wr; ++x)
-                    for (int32_t y = x + 1; y < wr; ++y) {
-                        const int bx = bank(row[x]), by = bank(row[y]);
-                        if (bx == by) continue;
-                        const int before = (cnt[size_t(x) * 32 + bx] > 1) + (cnt[size_t(y) * 32 + by] > 1);
-                        const int after = (cnt[size_t(x) * 32 + by] >= 1) + (cnt[size_t(y) * 32 + bx] >= 1);
-                        if (after < before) {
-                            cnt[size_t(x) * 32 + bx]--; cnt[size_t(y) * 32 + by]--;
-                            cnt[size_t(x) * 32 + by]++; cnt[size_t(y) * 32 + bx]++;
-                            std::swap(row[x], row[y]);
-                            any = true;
-                        }
-                    }
-            }
-            if (!any) break;
-        }
+        for (int32_t i = 0; i < nr; ++i)
+            for (int32_t j = 0; j < wr; ++j)
+                dst[size_t(i) * wr + col[size_t(i) * wr + j]] = rowsv[size_t(mem[size_t(i)]) * wr + j];
     }
     std::copy(out.begin(), out.end(), rowsv);
 }
@@ -340,7 +533,8 @@ double window_wavefronts(const int32_t *rowsv, int32_t wr, const std::vector<int
 
 void bank_balance_rows(int32_t n, int32_t wc, int32_t wr, std::vector<int32_t> &rel) {
     const int32_t mb = n / wr, NB = wc - 1;
-    if (wr > 32 || mb < 64) return;
+    // only the band kernels (a frame in one SM's shared memory) gather through this view
+    if (wr > 32 || mb < 64 || !band_frame_fits_sm(n, wc)) return;
     SplitMix64 rng(0x9e3779b97f4a7c15ull ^ uint64_t(n));
     for (int32_t b = 0; b < NB; ++b) {
         int32_t *band = rel.data() + size_t(b) * size_t(n);
