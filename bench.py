@@ -40,7 +40,8 @@ MUFU_PER_EDGE_UPDATE = 4
 KERNEL_NAMES = {1: "spa_decode_kernel (generic, on-chip)", 2: "spa_decode_kernel (generic, global state)",
                 3: "band_kernel (check-major E)", 4: "band_kernel (variable-major E)",
                 5: "band_cluster_kernel (L2 gathers)", 6: "band_kernel (variable-major E, 16-bit offsets)",
-                7: "xband_kernel (exchange cluster, bulk DSMEM segments)"}
+                7: "xband_kernel (exchange cluster, bulk DSMEM segments)",
+                8: "edge_kernel (lane per edge, small batches)"}
 
 
 def parse():

@@ -155,13 +155,17 @@ ldpc_status ldpc_encode(const ldpc_code *code, const uint32_t *d_info, uint32_t 
 /* The decoder variant ldpc_decode would run for these arguments (opts->variant
  * 0 resolved): 1 generic on-chip, 2 generic global-state, 3/4 Gallager band
  * kernel (check-/variable-major E), 5 cluster band kernel, 6 band kernel with
- * 16-bit offsets, 7 exchange cluster kernel.  *variant = 0 and
+ * 16-bit offsets, 7 exchange cluster kernel, 8 lane-per-edge small-batch
+ * kernel.  *variant = 0 and
  * LDPC_ERR_UNSUPPORTED when nothing fits. */
 ldpc_status ldpc_decode_variant(const ldpc_code *code, int64_t frames, const ldpc_decode_opts *opts,
                                 int32_t *variant);
 
 /* Workspace the chosen decode variant needs for `frames` frames (0 for the
- * on-chip variants; the large-n variants keep per-frame message state in it). */
+ * on-chip variants; the large-n variants keep per-frame message state in it).
+ * When auto resolves to variant 8 for a code the band kernel can decode, the
+ * band kernel's workspace is reported, so the same buffer serves
+ * ldpc_decode_simulate. */
 ldpc_status ldpc_decode_workspace_bytes(const ldpc_code *code, int64_t frames,
                                         const ldpc_decode_opts *opts, size_t *bytes);
 
@@ -186,11 +190,16 @@ ldpc_status ldpc_decode_workspace_bytes(const ldpc_code *code, int64_t frames,
  * early termination); 6 = 4 with 16-bit
  * offsets (n <= 16383); 7 exchange cluster kernel (same codes as 5; a
  * cluster of C CTAs per frame trades message segments with bulk DSMEM copies,
- * no workspace; fixed iterations, wr = 6).  Auto (0): a frame that fits one SM
- * runs the band kernel (one SM per frame) unless the batch is too small to
- * fill the GPU that way, in which case it runs variant 7 with C SMs per frame
- * (lower latency: stream mode, small batches); larger frames run 7, else 5;
- * any other H runs 1 or 2. */
+ * no workspace; fixed iterations, wr = 6); 8 lane-per-edge kernel (any H with
+ * row degree <= 32 whose E, L, R fit one SM's shared memory: a group of
+ * 4/8/16/32 lanes per check row, one CTA per frame, no workspace; for batches
+ * too small to fill the GPU with one thread per check row).  Auto (0): a
+ * frame that fits one SM runs the band kernel (one SM per frame) unless the
+ * batch is too small to fill the GPU that way, in which case it runs variant
+ * 7 with C SMs per frame when the code has that view (lower latency: stream
+ * mode, small batches), else variant 8 when there are no more frames than
+ * SMs; larger frames run 7, else 5; any other H runs 8 for such batches,
+ * else 1 or 2. */
 ldpc_status ldpc_decode(const ldpc_code *code, const float *d_llr, int64_t frames,
                         const ldpc_decode_opts *opts, uint32_t *d_bits,
                         uint8_t *d_syndrome_ok, int32_t *d_iters, float *d_posterior,
@@ -206,7 +215,9 @@ ldpc_status ldpc_decode(const ldpc_code *code, const float *d_llr, int64_t frame
  *   (ldpc_encode); d_bits / d_syndrome_ok / d_iters as ldpc_decode; no
  *   posterior.  Workspace: ldpc_decode_workspace_bytes for the same code,
  *   frames and opts.  Gallager (3,6) codes whose frame fits one SM, opts
- *   variant 0/3/4/6 (else LDPC_ERR_UNSUPPORTED); needs make_G before
+ *   variant 0/3/4/6 (else LDPC_ERR_UNSUPPORTED); it always runs the band
+ *   kernel (bit-identical to ldpc_decode with variant 3/4/6 as resolved for
+ *   the same opts, also where ldpc_decode's auto choice is variant 8); needs make_G before
  *   bind_device (LDPC_ERR_STATE); sigma > 0. */
 ldpc_status ldpc_decode_simulate(const ldpc_code *code, uint64_t seed, int64_t frame0, int64_t frames,
                                  double sigma, const uint32_t *d_info, const uint32_t *d_cw,

@@ -242,6 +242,23 @@ ldpc_status band_launch(const ldpc_code &c, const BandPlan &p, const float *llr,
                         const ldpc_decode_opts &o, uint32_t *bits, uint8_t *syn, int32_t *iters, float *post,
                         void *ws, size_t ws_bytes, void *stream);
 
+// Launch plan of the lane-per-edge small-batch decoder (spa_edge.cu; variant 8).
+struct EdgePlan {
+    void *kernel = nullptr;
+    int G = 0;                  // lanes per check row
+    int kc = 0;                 // rows per lane group
+    int threads = 0;
+    int grid = 0;
+    int64_t capacity = 0;       // frames decoded concurrently
+    size_t smem = 0;
+};
+// false when the code has a row of degree > 32 or a frame's E, L, R do not fit
+// one SM's shared memory.
+bool edge_plan(const ldpc_code &c, int64_t frames, bool et, int max_iter, EdgePlan &p);
+ldpc_status edge_launch(const ldpc_code &c, const EdgePlan &p, const float *llr, int64_t frames,
+                        const ldpc_decode_opts &o, uint32_t *bits, uint8_t *syn, int32_t *iters, float *post,
+                        void *stream);
+
 // Launch plan of the cluster band kernel (frames larger than one SM).
 struct ClusterPlan {
     void *kernel = nullptr;

@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "ldpc_internal.h"
 
@@ -475,6 +476,7 @@ namespace {
 // the L2-gather cluster kernel); the generic CSR kernels otherwise.
 struct Resolved {
     int variant = 0;
+    EdgePlan edge;
     BandPlan band;
     XClusterPlan x;
     ClusterPlan cl;
@@ -491,6 +493,28 @@ ldpc_status resolve(const ldpc_code &c, int64_t frames, const ldpc_decode_opts &
         r.variant = r.band.mode == 2 ? 6 : (r.band.vm ? 4 : 3);
         return LDPC_OK;
     }
+    if (v == 8) {
+        if (!edge_plan(c, frames, et, o.max_iter, r.edge)) return LDPC_ERR_UNSUPPORTED;
+        r.variant = 8;
+        return LDPC_OK;
+    }
+    // No more frames than SMs (stream mode): every frame has an SM to itself
+    // under either kernel, and the lane-per-edge kernel (a frame over G x more
+    // lanes) finishes it sooner where the band kernel leaves the SM's four
+    // schedulers idle (<= 2 warps per frame) or runs long serial chains (>= 64
+    // edges per thread and iteration); elsewhere, and with more frames per SM,
+    // its extra instructions per edge (padding lanes, shuffles, ballots) cost
+    // more than they save (measured).
+    const int64_t sms = device_attribute(cudaDevAttrMultiProcessorCount);
+    auto edge_small = [&](int64_t band_threads) {
+        if (v != 0 || std::getenv("LDPC_NO_EDGE") || frames > sms) return false;
+        if (band_threads > 0) {
+            const int64_t b0 = (c.dev.mb + band_threads - 1) / band_threads;
+            const int64_t chain = int64_t(c.dev.wc) * b0 * c.dev.wr;
+            if (band_threads > 64 && chain < 64) return false;
+        }
+        return edge_plan(c, frames, et, o.max_iter, r.edge);
+    };
     const bool x_ok = (v == 0 || v == 7) && xcluster_plan(c, frames, et, r.x);
     if (v == 7) {
         if (!x_ok) return LDPC_ERR_UNSUPPORTED;
@@ -509,6 +533,10 @@ ldpc_status resolve(const ldpc_code &c, int64_t frames, const ldpc_decode_opts &
                 return LDPC_OK;
             }
         }
+        if (edge_small(r.band.threads)) {
+            r.variant = 8;
+            return LDPC_OK;
+        }
         r.variant = r.band.mode == 2 ? 6 : (r.band.vm ? 4 : 3);
         return LDPC_OK;
     }
@@ -522,6 +550,10 @@ ldpc_status resolve(const ldpc_code &c, int64_t frames, const ldpc_decode_opts &
             return LDPC_OK;
         }
         if (v == 5) return LDPC_ERR_UNSUPPORTED;
+    }
+    if (edge_small(0)) {
+        r.variant = 8;
+        return LDPC_OK;
     }
     const ldpc_status s = make_plan(c, frames, o, r.gen);
     if (s != LDPC_OK) return s;
@@ -553,6 +585,9 @@ ldpc_status ldpc_decode_workspace_bytes(const ldpc_code *code, int64_t frames, c
         case 3: case 4: case 6: *bytes = r.band.ws_bytes; break;
         case 7: *bytes = r.x.ws_bytes; break;
         case 5: *bytes = r.cl.ws_bytes; break;
+        // variant 8 needs none; where the band kernel could decode the code, its
+        // workspace is reported so one buffer also serves ldpc_decode_simulate
+        case 8: *bytes = r.band.kernel ? r.band.ws_bytes : 0; break;
         default: *bytes = r.gen.ws_bytes; break;
     }
     return LDPC_OK;
@@ -577,6 +612,9 @@ ldpc_status ldpc_decode(const ldpc_code *code, const float *d_llr, int64_t frame
         case 7:
             return ldpc::xcluster_launch(*code, r.x, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters,
                                          d_posterior, stream);
+        case 8:
+            return ldpc::edge_launch(*code, r.edge, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters, d_posterior,
+                                     stream);
         case 5:
             return ldpc::cluster_launch(*code, r.cl, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters,
                                         d_posterior, d_ws, ws_bytes, stream);
