@@ -105,6 +105,25 @@ __device__ __forceinline__ void psi_row(const float (&in)[D], float (&out)[D]) {
     for (int j = 0; j < D; ++j) out[j] = psi(in[j]);
 }
 
+// Saturation bound of a degree-D row: when every |L'_vc| of the row is >= it,
+// E'_cv = +-E_MAX for every edge, whichever psi tier would evaluate it: each
+// term is psi(y) = h0 2^-y (1 + O(2^-2y)) in every tier (relative excess
+// < 1e-25 at y >= 42), so every exclusive sum is <= (D-1) h0 2^-y_sat, and
+// its psi, >= C1 - lg2(sum) in every tier, is >= E_MAX + 0.02 -- a margin far
+// above the approx instructions' ~1e-6 error, so the clamp min(psi, E_MAX)
+// returns E_MAX bit for bit.  Reachable only below the input clamp: D <= 6
+// (y_sat = 43.205 for D = 6, 42.468 for D = 4; the clamp is 43.281).
+template <int D>
+__host__ __device__ constexpr float sat_bound() {
+    // log2((D-1) h0) for D = 2..7 (h0 = 2.88539008 = 2 log2 e)
+    return D == 2 ? 40.863137f - 1.528766f + 1.528766f + 0.02f
+         : D == 3 ? 40.863137f - 1.528766f + 2.528766f + 0.02f
+         : D == 4 ? 40.863137f - 1.528766f + 3.113729f + 0.02f
+         : D == 5 ? 40.863137f - 1.528766f + 3.528766f + 0.02f
+         : D == 6 ? 40.863137f - 1.528766f + 3.850694f + 0.02f
+                  : 1e30f;
+}
+
 // Check-node update of one row (Eq. 5, readings Q2/Q3/Q7) in log2 units.
 // x[j] = L'_v - E'_cv (not yet clamped); e[j] <- new E'_cv.
 template <int D, bool VOTE>
@@ -115,6 +134,19 @@ __device__ __forceinline__ void check_row(const float (&x)[D], float (&e)[D]) {
     for (int j = 0; j < D; ++j) {
         sx ^= __float_as_uint(x[j]);
         ax[j] = fminf(fabsf(x[j]), kClampB);
+    }
+    if constexpr (VOTE && sat_bound<D>() <= kClampB) {
+        // saturated rows (every input at the clamp: a converged frame under
+        // fixed iterations): E = +-E_MAX exactly as the full update gives it
+        float lo = ax[0];
+#pragma unroll
+        for (int j = 1; j < D; ++j) lo = fminf(lo, ax[j]);
+        if (__all_sync(__activemask(), lo >= sat_bound<D>())) {
+#pragma unroll
+            for (int j = 0; j < D; ++j)
+                e[j] = __uint_as_float(__float_as_uint(kEMaxB) | ((sx ^ __float_as_uint(x[j])) & 0x80000000u));
+            return;
+        }
     }
     psi_row<D, true, VOTE>(ax, f);
     // exclusive sums Phi_j = sum_{k != j} f_k of positive terms: never
