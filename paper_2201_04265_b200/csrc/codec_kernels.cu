@@ -117,6 +117,41 @@ __global__ void __launch_bounds__(256) encode_assemble_kernel(const DeviceCode c
     }
 }
 
+// Small codes (k <= 128 bits) in small batches: the tiled kernel's 64-frame
+// x 128-column tiles and 32-word k chunks are mostly padding there (C1: k =
+// 48, two words), so one kernel does both steps, one warp per frame: lane i
+// holds message word i, and each output bit v (H column order) is either a
+// message bit or parity column c = pinv[v] - k, the GF(2) dot product of the
+// message with column c of P (popc of kw ANDed words); bits are packed by
+// ballot.  Same result as parity + assemble (tests/test_gpu_parity.py).
+__global__ void __launch_bounds__(256) encode_small_kernel(const DeviceCode code, const uint32_t *__restrict__ info,
+                                                           uint32_t *__restrict__ cw, int64_t frames) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wg = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    const int kw = code.kw, nw = code.nw, k = code.k, n = code.n, npp = code.npar_pad;
+    for (int64_t f = wg; f < frames; f += nwarps) {
+        const uint32_t mine = lane < kw ? __ldg(info + f * int64_t(kw) + lane) : 0u;
+        uint32_t *row = cw + f * int64_t(nw);
+        for (int v0 = 0; v0 < nw * 32; v0 += 32) {
+            const int v = v0 + lane;
+            const int t = v < n ? __ldg(code.pinv + v) : -1;
+            // parity column t - k: every lane takes part in the shuffles
+            uint32_t acc = 0u;
+            for (int w = 0; w < kw; ++w) {
+                const uint32_t mw = __shfl_sync(0xffffffffu, mine, w);
+                if (t >= k) acc ^= mw & __ldg(code.pt + size_t(w) * npp + (t - k));
+            }
+            uint32_t bit = uint32_t(__popc(acc)) & 1u;
+            // message bits: word t >> 5 from its lane (every lane takes part)
+            const uint32_t mw = __shfl_sync(0xffffffffu, mine, t >= 0 && t < k ? (t >> 5) : 0);
+            if (t >= 0 && t < k) bit = (mw >> (t & 31)) & 1u;
+            const uint32_t word = __ballot_sync(0xffffffffu, bit != 0u);
+            if (lane == 0) row[v0 >> 5] = word;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Info bits: one thread per 4 words = one Philox block (counter (w/4, f, 0)).
 __global__ void gen_info_kernel(uint64_t seed, int64_t frame0, int64_t frames, int k, uint32_t *out) {
@@ -243,6 +278,13 @@ ldpc_status ldpc_encode(const ldpc_code *code, const uint32_t *d_info, uint32_t 
     if (!d_info || !d_cw) return LDPC_ERR_ARG;
     const ldpc::DeviceCode &D = code->dev;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // measured: C1 (kw = 2) 11.4 -> 6 us cold; at kw = 9..25 (Table I) the
+    // per-lane scattered P loads made it 10x slower than the tiled path
+    if (D.kw <= 4 && frames * int64_t(D.n) * D.kw <= (int64_t(1) << 26)) {
+        const int grid = int(std::min<int64_t>((frames + 7) / 8, int64_t(ldpc::sm_count()) * 16));
+        ldpc::encode_small_kernel<<<dim3(unsigned(std::max(grid, 1))), 256, 0, s>>>(D, d_info, d_cw, frames);
+        return cudaGetLastError() == cudaSuccess ? LDPC_OK : LDPC_ERR_CUDA;
+    }
     const unsigned col_tiles = unsigned(D.npar_pad / ldpc::kEncColTile);
     const int64_t max_chunk = int64_t(65535) * ldpc::kEncTF;      // gridDim.y limit
     for (int64_t f0 = 0; f0 < frames && col_tiles > 0; f0 += max_chunk) {
