@@ -188,6 +188,104 @@ __device__ __forceinline__ void check_row(const float (&x)[D], float (&e)[D]) {
     }
 }
 
+// check_row split over a lane pair (band_kernel LPR = 2): lane h = lane & 1
+// holds elements [h D/2, (h+1) D/2) of the row (x, e of D/2 entries); its
+// partner is lane ^ 1 of the same warp.  The exclusive sums reproduce
+// check_row's association exactly (pairwise tree for D = 4, 6; prefix and
+// suffix otherwise, each half continuing the other's running sum), so
+// without psi votes a row decodes bit for bit as in check_row.
+// pm: the warp's lanes running this call (both lanes of every pair).
+template <int D, bool VOTE>
+__device__ __forceinline__ void check_row_pair(const float (&x)[D / 2], float (&e)[D / 2], int h, unsigned pm) {
+    constexpr int W = D / 2;
+    static_assert(D % 2 == 0, "lane pairs split even degrees");
+    float f[W], ax[W];
+    uint32_t sl = 0;
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        sl ^= __float_as_uint(x[j]);
+        ax[j] = fminf(fabsf(x[j]), kClampB);
+    }
+    const uint32_t sx = sl ^ __shfl_xor_sync(pm, sl, 1) ^ ((D & 1) ? 0x80000000u : 0u);
+    if constexpr (VOTE && sat_bound<D>() <= kClampB) {
+        float lo = ax[0];
+#pragma unroll
+        for (int j = 1; j < W; ++j) lo = fminf(lo, ax[j]);
+        if (__all_sync(__activemask(), lo >= sat_bound<D>())) {
+#pragma unroll
+            for (int j = 0; j < W; ++j)
+                e[j] = __uint_as_float(__float_as_uint(kEMaxB) | ((sx ^ __float_as_uint(x[j])) & 0x80000000u));
+            return;
+        }
+    }
+    psi_row<W, true, VOTE>(ax, f);
+    float ex[W];
+    if constexpr (D == 6) {
+        // half 0: f0 f1 f2, half 1: f3 f4 f5; a01 + a45 etc. as check_row<6>
+        const float mine = h ? f[0] : f[2];                        // f3 / f2
+        const float other = __shfl_xor_sync(pm, mine, 1);  // f2 / f3
+        const float pr = h ? f[1] + f[2] : f[0] + f[1];             // a45 / a01
+        const float opr = __shfl_xor_sync(pm, pr, 1);      // a01 / a45
+        const float a23 = h ? other + f[0] : f[2] + other;          // f2 + f3
+        if (h == 0) {
+            const float o01 = a23 + opr;      // a23 + a45
+            const float o23 = pr + opr;       // a01 + a45
+            ex[0] = f[1] + o01;
+            ex[1] = f[0] + o01;
+            ex[2] = other + o23;              // f3 + o23
+        } else {
+            const float o23 = opr + pr;       // a01 + a45
+            const float o45 = opr + a23;      // a01 + a23
+            ex[0] = other + o23;              // f2 + o23
+            ex[1] = f[2] + o45;               // f5 + o45
+            ex[2] = f[1] + o45;               // f4 + o45
+        }
+    } else if constexpr (D == 4) {
+        const float pr = f[0] + f[1];
+        const float opr = __shfl_xor_sync(pm, pr, 1);
+        ex[0] = f[1] + opr;
+        ex[1] = f[0] + opr;
+    } else {
+        // forward sum of half 0 and backward sum of half 1, exchanged
+        float fw = 0.0f, bw = 0.0f;
+#pragma unroll
+        for (int j = 0; j < W; ++j) fw += f[j];
+#pragma unroll
+        for (int j = W - 1; j >= 0; --j) bw += f[j];
+        const float got = __shfl_xor_sync(pm, h ? bw : fw, 1);
+        float acc = h ? got : 0.0f;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            ex[j] = acc;
+            acc += f[j];
+        }
+        acc = h ? 0.0f : got;
+#pragma unroll
+        for (int j = W - 1; j >= 0; --j) {
+            ex[j] += acc;
+            acc += f[j];
+        }
+    }
+    float g[W];
+    psi_row<W, false, VOTE>(ex, g);
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+        const float mag = fminf(g[j], kEMaxB);
+        const uint32_t sgn = (sx ^ __float_as_uint(x[j])) & 0x80000000u;
+        e[j] = __uint_as_float(__float_as_uint(mag) | sgn);
+    }
+}
+
+// One row's update by one lane (LPR = 1) or a lane pair (LPR = 2).
+template <int D, bool VOTE, int LPR>
+__device__ __forceinline__ void check_any(const float (&x)[D / LPR], float (&e)[D / LPR], int h, unsigned pm) {
+    if constexpr (LPR == 1) {
+        check_row<D, VOTE>(x, e);
+    } else {
+        check_row_pair<D, VOTE>(x, e, h, pm);
+    }
+}
+
 template <int D>
 __device__ __forceinline__ void lds_row(const char *smem, uint32_t byte_off, float (&o)[D]) {
     const float *p = reinterpret_cast<const float *>(smem + byte_off);

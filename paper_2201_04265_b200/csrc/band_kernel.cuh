@@ -53,19 +53,31 @@ __device__ __forceinline__ bool cta_sync_or(bool p) { return __syncthreads_or(p 
 // after a frame has converged; with few iterations (C1: 20, Table I: 10) they
 // are overhead and their branches and warp syncs lengthen the dependency
 // chain (measured: C1 +35%, Table I +6..20%).  Chosen at plan time.
-template <int WR, int WC, int B0, bool ET, int MODE, int NFIX = 0, bool GEN = false, int RPRE = 0, bool NOVOTE = false>
-__global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const BandArgs a) {
+// LPR: lanes per check row.  2 splits every row over a lane pair (each lane
+// WR/2 elements, check_row_pair): twice the threads per frame and half the
+// serial chain, for batches too small to fill the GPU one thread per row
+// (C1, Table I at 1000 frames).  Without psi votes the results are bit for
+// bit those of LPR = 1.  NFIX kernels only.
+template <int WR, int WC, int B0, bool ET, int MODE, int NFIX = 0, bool GEN = false, int RPRE = 0, bool NOVOTE = false,
+          int LPR = 1>
+__global__ void __launch_bounds__(WC > 3 ? 256 * LPR : 1024, 1) band_kernel(const BandArgs a) {
     // measured on B200: +1.1 points on C4 (MODE 2), +0.8..1.3 on wr = 12 codes,
     // -2..3 on check-major wr = 4 / 6 codes (C3 R1/4, R1/2)
     constexpr bool FUSE0 = BAND_FUSE0 && (MODE == 2 || WR >= 12 || NOVOTE);
     constexpr bool VM = MODE >= 1, L16 = MODE == 2;
+    static_assert(LPR == 1 || (LPR == 2 && NFIX && !GEN && RPRE == 0 && WR % 2 == 0), "lane pairs: NFIX kernels");
+    constexpr int WH = WR / LPR;          // elements of a row per lane
     extern __shared__ __align__(16) char smem[];
     __shared__ long long s_frame;
     const DeviceCode &code = a.code;
+    // rows per row-pass (the row stride, a multiple of 32) and threads
+    // (= TFIX * LPR): lane pairs double the threads of the same row passes
     constexpr int TFIX = NFIX ? (((NFIX / WR + B0 - 1) / B0 + 31) / 32 * 32) : 0;
     constexpr bool RFIX_SMEM = NFIX && size_t(WC + 1) * NFIX * 4 + 1024 <= 227 * 1024;
     const int n = NFIX ? NFIX : code.n, mb = NFIX ? NFIX / WR : code.mb;
-    const int T = NFIX ? TFIX : int(blockDim.x), tt = threadIdx.x, S = NFIX ? TFIX : a.row_stride;
+    const int T = NFIX ? TFIX * LPR : int(blockDim.x), tt = threadIdx.x, S = NFIX ? TFIX : a.row_stride;
+    const int pr = tt / LPR, h = tt % LPR;   // row slot, half of the row
+    const uint32_t hoff = uint32_t(h * WH);  // first element of this lane
     const bool r_in_smem = NFIX ? RFIX_SMEM : a.r_in_smem != 0;
     constexpr int NB = WC - 1;          // bands held in shared memory
     constexpr int B1 = NB * B0;         // max rows of bands >= 1 per thread
@@ -116,11 +128,11 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
         }
         for (int i = tt; i < (NB * n) >> 2; i += T)
             reinterpret_cast<float4 *>(smem)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        float e0[B0][WR];
+        float e0[B0][WH];
 #pragma unroll
         for (int k = 0; k < B0; ++k)
 #pragma unroll
-            for (int j = 0; j < WR; ++j) e0[k][j] = 0.0f;
+            for (int j = 0; j < WH; ++j) e0[k][j] = 0.0f;
         __syncthreads();
 
         int32_t iters = a.max_iter;
@@ -134,11 +146,13 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
         if constexpr (FUSE0) {
 #pragma unroll
             for (int k = 0; k < B0; ++k) {
-                const int r = tt + k * S;
-                if (tt < S && r < mb) {
-                    float x[WR];
-                    lds_row<WR>(smem, lbase + uint32_t(r) * WR * 4u, x);
-                    check_row<WR, !ET && !NOVOTE>(x, e0[k]);
+                const int r = pr + k * S;
+                const bool act = pr < S && r < mb;
+                const unsigned pm = LPR > 1 ? __ballot_sync(0xffffffffu, act) : 0u;
+                if (act) {
+                    float x[WH];
+                    lds_row<WH>(smem, lbase + (uint32_t(r) * WR + hoff) * 4u, x);
+                    check_any<WR, !ET && !NOVOTE, LPR>(x, e0[k], h, pm);
                 }
             }
         }
@@ -147,27 +161,36 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
             uint32_t synd = FUSE0 ? synd0 : 0u;
 #pragma unroll
             for (int k = 0; k < (FUSE0 ? 0 : B0); ++k) {
-                const int r = tt + k * S;
-                if (tt < S && r < mb) {
-                    float lv[WR], x[WR];
-                    lds_row<WR>(smem, lbase + uint32_t(r) * WR * 4u, lv);
+                const int r = pr + k * S;
+                const bool act = pr < S && r < mb;
+                const unsigned pm = LPR > 1 ? __ballot_sync(0xffffffffu, act) : 0u;
+                if (act) {
+                    float lv[WH], x[WH];
+                    lds_row<WH>(smem, lbase + (uint32_t(r) * WR + hoff) * 4u, lv);
                     uint32_t rp = 0;      // this row's syndrome bit (Eq. 1)
 #pragma unroll
-                    for (int j = 0; j < WR; ++j) {
+                    for (int j = 0; j < WH; ++j) {
                         x[j] = lv[j] - e0[k][j];
                         if (ET) rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
                     }
+                    if (ET && LPR > 1) rp ^= __shfl_xor_sync(pm, rp, 1);
                     synd |= rp;
-                    check_row<WR, !ET && !NOVOTE>(x, e0[k]);
+                    check_any<WR, !ET && !NOVOTE, LPR>(x, e0[k], h, pm);
                 }
             }
 #pragma unroll
             for (int k = 0; k < B1; ++k) {
-                const int r = tt + k * S;
-                if (tt < S && r < NB * mb) {
-                    int32_t li[WR];
-                    float e[WR], x[WR];
-                    if (L16) {
+                const int r = pr + k * S;
+                const bool act = pr < S && r < NB * mb;
+                const unsigned pm = LPR > 1 ? __ballot_sync(0xffffffffu, act) : 0u;
+                if (act) {
+                    int32_t li[WH];
+                    float e[WH], x[WH];
+                    if (L16 && LPR > 1) {
+#pragma unroll
+                        for (int j = 0; j < WH; ++j)
+                            li[j] = int32_t(lbase + __ldg(code.band_lidx16 + size_t(r) * WR + hoff + j));
+                    } else if (L16) {
                         // 16-bit offsets relative to L: half the index bytes through L1/L2
                         const uint32_t *p16 = reinterpret_cast<const uint32_t *>(code.band_lidx16 + size_t(r) * WR);
 #pragma unroll
@@ -177,30 +200,31 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
                             li[2 * w + 1] = int32_t(lbase + (x >> 16));
                         }
                     } else {
-                        ldg_idx<WR>(lidx + size_t(r) * WR, li);
+                        ldg_idx<WH>(lidx + size_t(r) * WR + hoff, li);
                     }
                     // VM: E_b is variable-major, at the variable's L offset + delta_b
                     const int32_t delta = VM ? int32_t((r / mb) * n * 4) - int32_t(lbase) : 0;
                     if (VM) {
 #pragma unroll
-                        for (int j = 0; j < WR; ++j) e[j] = *reinterpret_cast<const float *>(smem + li[j] + delta);
+                        for (int j = 0; j < WH; ++j) e[j] = *reinterpret_cast<const float *>(smem + li[j] + delta);
                     } else {
-                        lds_row<WR>(smem, uint32_t(r) * WR * 4u, e);
+                        lds_row<WH>(smem, (uint32_t(r) * WR + hoff) * 4u, e);
                     }
                     uint32_t rp = 0;
 #pragma unroll
-                    for (int j = 0; j < WR; ++j) {
+                    for (int j = 0; j < WH; ++j) {
                         const float lv = *reinterpret_cast<const float *>(smem + li[j]);
                         x[j] = lv - e[j];
                         if (ET) rp ^= (lv >= 0.0f) ? 1u : 0u;
                     }
+                    if (ET && LPR > 1) rp ^= __shfl_xor_sync(pm, rp, 1);
                     synd |= rp;
-                    check_row<WR, !ET && !NOVOTE>(x, e);
+                    check_any<WR, !ET && !NOVOTE, LPR>(x, e, h, pm);
                     if (VM) {
 #pragma unroll
-                        for (int j = 0; j < WR; ++j) *reinterpret_cast<float *>(smem + li[j] + delta) = e[j];
+                        for (int j = 0; j < WH; ++j) *reinterpret_cast<float *>(smem + li[j] + delta) = e[j];
                     } else {
-                        sts_row<WR>(smem, uint32_t(r) * WR * 4u, e);
+                        sts_row<WH>(smem, (uint32_t(r) * WR + hoff) * 4u, e);
                     }
                 }
             }
@@ -212,8 +236,8 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
             if (RP > 0 && !r_in_smem) {
 #pragma unroll
                 for (int k = 0; k < RP; ++k) {
-                    const int r = tt + k * S;
-                    if (tt < S && r < mb) lds_row<WR>(reinterpret_cast<const char *>(Rs), uint32_t(r) * WR * 4u, rpre[k]);
+                    const int r = pr + k * S;
+                    if (pr < S && r < mb) lds_row<WR>(reinterpret_cast<const char *>(Rs), uint32_t(r) * WR * 4u, rpre[k]);
                 }
             }
             if (ET) {
@@ -230,50 +254,53 @@ __global__ void __launch_bounds__(WC > 3 ? 256 : 1024, 1) band_kernel(const Band
             synd0 = 0;
 #pragma unroll
             for (int k = 0; k < B0; ++k) {
-                const int r = tt + k * S;
-                if (tt < S && r < mb) {
-                    float rv[WR], lv[WR];
+                const int r = pr + k * S;
+                const bool act = pr < S && r < mb;
+                const unsigned pm = LPR > 1 ? __ballot_sync(0xffffffffu, act) : 0u;
+                if (act) {
+                    float rv[WH], lv[WH];
                     if (k < RP && !r_in_smem) {
 #pragma unroll
-                        for (int j = 0; j < WR; ++j) rv[j] = rpre[k < RP ? k : 0][j];
+                        for (int j = 0; j < WH; ++j) rv[j] = rpre[k < RP ? k : 0][j];
                     } else {
-                        lds_row<WR>(reinterpret_cast<const char *>(Rs), uint32_t(r) * WR * 4u, rv);
+                        lds_row<WH>(reinterpret_cast<const char *>(Rs), (uint32_t(r) * WR + hoff) * 4u, rv);
                     }
                     if (VM) {
                         // this row's variables are contiguous in every band's E_b
 #pragma unroll
-                        for (int j = 0; j < WR; ++j) lv[j] = rv[j] + e0[k][j];
+                        for (int j = 0; j < WH; ++j) lv[j] = rv[j] + e0[k][j];
 #pragma unroll
                         for (int b = 0; b < NB; ++b) {
-                            float eb[WR];
-                            lds_row<WR>(smem, uint32_t(b) * n * 4u + uint32_t(r) * WR * 4u, eb);
+                            float eb[WH];
+                            lds_row<WH>(smem, uint32_t(b) * n * 4u + (uint32_t(r) * WR + hoff) * 4u, eb);
 #pragma unroll
-                            for (int j = 0; j < WR; ++j) lv[j] += eb[j];
+                            for (int j = 0; j < WH; ++j) lv[j] += eb[j];
                         }
                     } else {
-                        int32_t vp[WR * NB];
-                        ldg_idx<WR * NB>(vpos + size_t(r) * WR * NB, vp);
+                        int32_t vp[WH * NB];
+                        ldg_idx<WH * NB>(vpos + (size_t(r) * WR + hoff) * NB, vp);
 #pragma unroll
-                        for (int j = 0; j < WR; ++j) {
+                        for (int j = 0; j < WH; ++j) {
                             float s = rv[j] + e0[k][j];
 #pragma unroll
                             for (int b = 0; b < NB; ++b) s += *reinterpret_cast<const float *>(smem + vp[j * NB + b]);
                             lv[j] = s;
                         }
                     }
-                    sts_row<WR>(smem, lbase + uint32_t(r) * WR * 4u, lv);
+                    sts_row<WH>(smem, lbase + (uint32_t(r) * WR + hoff) * 4u, lv);
                     if constexpr (FUSE0) {
                         if (ET) {
                             uint32_t rp = 0;      // this band-0 row's syndrome bit of z^t (Eq. 1)
 #pragma unroll
-                            for (int j = 0; j < WR; ++j) rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
+                            for (int j = 0; j < WH; ++j) rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
+                            if (LPR > 1) rp ^= __shfl_xor_sync(pm, rp, 1);
                             synd0 |= rp;
                         }
                         if (t < a.max_iter) {
-                            float x[WR];
+                            float x[WH];
 #pragma unroll
-                            for (int j = 0; j < WR; ++j) x[j] = lv[j] - e0[k][j];
-                            check_row<WR, !ET && !NOVOTE>(x, e0[k]);
+                            for (int j = 0; j < WH; ++j) x[j] = lv[j] - e0[k][j];
+                            check_any<WR, !ET && !NOVOTE, LPR>(x, e0[k], h, pm);
                         }
                     }
                 }

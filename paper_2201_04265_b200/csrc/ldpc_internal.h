@@ -224,14 +224,18 @@ struct BandPlan {
     bool r_in_smem = false;
     bool vm = false;            // E of bands >= 1 stored variable-major
     int mode = 0;               // kernel MODE: 0 check-major, 1 VM, 2 VM + 16-bit offsets
+    int lpr = 1;                // lanes per check row (2: lane-pair kernel, small batches)
     size_t ws_bytes = 0;
 };
 // false when the code is not eligible (not from ldpc_make_H, unsupported
 // (wc, wr), n % 4 != 0, or the frame does not fit one SM's shared memory).
 // variant: 0 auto, 3 check-major E, 4 variable-major E.
-bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPlan &p, int max_iter = 50);
+// lane_pairs: allow the LPR = 2 kernels (the fused simulate path has none).
+bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPlan &p, int max_iter = 50,
+               bool lane_pairs = true);
 // band_kernel instantiation with n compiled in (spa_band_fixed.cu), or nullptr.
-void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode, int max_iter);
+// lpr: lanes per check row (1, or 2 for the lane-pair instantiations).
+void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode, int max_iter, int lpr = 1);
 // Whether the band decoder runs without psi regime votes for this code and
 // iteration count (few-iteration configs with a compile-time-n kernel).
 inline bool band_novote(int n, int wr, int wc, int max_iter, bool et) {

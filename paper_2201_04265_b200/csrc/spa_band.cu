@@ -361,7 +361,7 @@ ldpc_status cluster_launch(const ldpc_code &c, const ClusterPlan &p, const float
     return e == cudaSuccess ? LDPC_OK : LDPC_ERR_CUDA;
 }
 
-bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPlan &p, int max_iter) {
+bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPlan &p, int max_iter, bool lane_pairs) {
     if (!c.gallager || !c.regular_col || (c.n & 3)) return false;
     const int mb = c.n / c.wr;
     const int sms = device_attribute(cudaDevAttrMultiProcessorCount);
@@ -379,12 +379,30 @@ bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPla
     p.vm = variant == 4 || variant == 6 || (variant == 0 && (!p.r_in_smem || c.wc > 3));
     // 16-bit offsets (variant 6, auto with VM when n <= 16383): +2% on C4
     p.mode = p.vm ? (((variant == 6 || variant == 0) && c.n <= 16383) ? 2 : 1) : 0;
-    void *k = std::getenv("LDPC_NO_NFIX") ? nullptr : pick_band_kernel_fixed(c.n, c.wr, c.wc, b0, et, p.mode, max_iter);
+    p.threads = ((mb + b0 - 1) / b0 + 31) / 32 * 32;
+    // Small batches (frames x threads under half the GPU's resident threads)
+    // of codes with long per-thread chains (wc x wr >= 64 edges per thread
+    // and iteration: Table I R1/4, R1/2 at 1000 frames) are latency-bound:
+    // split every check row over a lane pair (LPR = 2) -- twice the warps per
+    // frame, half the chain per thread; without psi votes bit for bit the
+    // same results.  Measured: T1-R1/4 29 -> 40%, T1-R1/2 33 -> 42% of the
+    // SFU roofline; C1 (18 edges per thread) -3%, so not used there.
+    p.lpr = 1;
+    void *k = nullptr;
+    const bool nfix = !std::getenv("LDPC_NO_NFIX");
+    if (lane_pairs && nfix && !std::getenv("LDPC_NO_LPR2") && frames * p.threads < int64_t(sms) * 1024 &&
+        c.wc * c.wr >= 64) {
+        k = pick_band_kernel_fixed(c.n, c.wr, c.wc, b0, et, p.mode, max_iter, 2);
+        if (k) {
+            p.lpr = 2;
+            p.threads *= 2;
+        }
+    }
+    if (!k && nfix) k = pick_band_kernel_fixed(c.n, c.wr, c.wc, b0, et, p.mode, max_iter);
     if (!k) k = pick_band_kernel(c.wr, c.wc, b0, et, p.mode);
     if (!k) return false;
     p.smem = p.r_in_smem ? with_r : base;
-    p.threads = ((mb + b0 - 1) / b0 + 31) / 32 * 32;
-    if (p.threads > (c.wc > 3 ? 256 : 1024)) return false;        // the kernel's launch bound
+    if (p.threads > (c.wc > 3 ? 256 * p.lpr : 1024)) return false;    // the kernel's launch bound
     p.kernel = k;
     if (!ensure_smem_attribute(k, p.smem)) return false;
     const int per_sm = occupancy_blocks(k, p.threads, p.smem);
@@ -415,7 +433,7 @@ ldpc_status band_launch(const ldpc_code &c, const BandPlan &p, const float *llr,
     a.r_in_smem = p.r_in_smem ? 1 : 0;
     // Row stride = block size.  (A stride of exactly ceil(mb / B0), which gives
     // every thread the same row count, measured 1.7 points slower on C4.)
-    a.row_stride = p.threads;
+    a.row_stride = p.threads / p.lpr;
     if (cudaMemsetAsync(ws, 0, 8, s) != cudaSuccess) return LDPC_ERR_CUDA;
     void *args[] = {&a};
     cudaError_t e = cudaLaunchKernel(p.kernel, dim3(unsigned(p.grid)), dim3(unsigned(p.threads)), args, p.smem, s);

@@ -37,8 +37,25 @@ void *et_pair_nv(bool et, bool novote) {
 //   check-major; Table I 1032 (wc 9/6 VM+16-bit, 3 check-major).  Measured
 //   on B200 against NFIX = 0: C2 +2.6, C4 +2.9, C3-R3/4 +0.7, Table I R1/4
 //   (100k frames) +1.3 points of the SFU roofline; C3 (3,4) -0.7 (left out).
-void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode, int max_iter) {
+// Lane-pair kernels (LPR = 2): Table I R1/4 and R1/2 in small batches.
+template <int WR, int WC, int MODE, int N>
+void *lpr2(bool et, bool novote) {
+    if (et) return reinterpret_cast<void *>(&band_kernel<WR, WC, 1, true, MODE, N, false, 0, false, 2>);
+    if (novote) return reinterpret_cast<void *>(&band_kernel<WR, WC, 1, false, MODE, N, false, 0, true, 2>);
+    return reinterpret_cast<void *>(&band_kernel<WR, WC, 1, false, MODE, N, false, 0, false, 2>);
+}
+
+void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode, int max_iter, int lpr) {
     const bool novote = band_novote(n, wr, wc, max_iter, et);
+    if (lpr == 2) {
+        if (b0 != 1) return nullptr;
+        if (wr == 12 && n == 1032) {
+            if (wc == 9 && mode == 2) return lpr2<12, 9, 2, 1032>(et, novote);
+            if (wc == 6 && mode == 2) return lpr2<12, 6, 2, 1032>(et, novote);
+        }
+        return nullptr;
+    }
+    if (lpr != 1) return nullptr;
     if (wc == 3 && wr == 6 && n == 16200 && b0 == 3 && mode == 2) {
         // R of 2 of the 3 band-0 rows prefetched before the check->variable
         // barrier (RPRE; measured on B200: 0 rows 65.8%, 1 67.2%, 2 68.2%,

@@ -57,7 +57,7 @@ extern "C" ldpc_status ldpc_decode_simulate(const ldpc_code *code, uint64_t seed
     const int v = opts->variant;
     if (v != 0 && v != 3 && v != 4 && v != 6) return LDPC_ERR_UNSUPPORTED;
     ldpc::BandPlan bp;
-    if (!ldpc::band_plan(*code, frames, opts->early_term != 0, v, bp, opts->max_iter)) return LDPC_ERR_UNSUPPORTED;
+    if (!ldpc::band_plan(*code, frames, opts->early_term != 0, v, bp, opts->max_iter, false)) return LDPC_ERR_UNSUPPORTED;
     const int b0 = std::max(1, (code->n / code->wr + 1023) / 1024);
     void *k = ldpc::pick_gen_kernel(code->n, code->wr, code->wc, b0, opts->early_term != 0, bp.mode, opts->max_iter);
     if (!k) return LDPC_ERR_UNSUPPORTED;
