@@ -380,18 +380,16 @@ bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPla
     // 16-bit offsets (variant 6, auto with VM when n <= 16383): +2% on C4
     p.mode = p.vm ? (((variant == 6 || variant == 0) && c.n <= 16383) ? 2 : 1) : 0;
     p.threads = ((mb + b0 - 1) / b0 + 31) / 32 * 32;
-    // Small batches (frames x threads under half the GPU's resident threads)
-    // of codes with long per-thread chains (wc x wr >= 64 edges per thread
-    // and iteration: Table I R1/4, R1/2 at 1000 frames) are latency-bound:
-    // split every check row over a lane pair (LPR = 2) -- twice the warps per
-    // frame, half the chain per thread; without psi votes bit for bit the
-    // same results.  Measured: T1-R1/4 29 -> 40%, T1-R1/2 33 -> 42% of the
-    // SFU roofline; C1 (18 edges per thread) -3%, so not used there.
+    // Codes with long per-thread chains (wc x wr >= 64 edges per thread and
+    // iteration: Table I R1/4, R1/2) split every check row over a lane pair
+    // (LPR = 2): twice the warps per frame, half the chain per thread, more
+    // warps per SM where shared memory caps the CTAs; without psi votes bit
+    // for bit the same results.  Measured (SFU roofline): T1-R1/4 29 -> 40%
+    // at 1000 frames, 39 -> 47% at 100k; T1-R1/2 33 -> 42%, 39 -> 52%.
     p.lpr = 1;
     void *k = nullptr;
     const bool nfix = !std::getenv("LDPC_NO_NFIX");
-    if (lane_pairs && nfix && !std::getenv("LDPC_NO_LPR2") && frames * p.threads < int64_t(sms) * 1024 &&
-        c.wc * c.wr >= 64) {
+    if (lane_pairs && nfix && !std::getenv("LDPC_NO_LPR2") && (c.wc * c.wr >= 64 || std::getenv("LDPC_LPR2_ALL"))) {
         k = pick_band_kernel_fixed(c.n, c.wr, c.wc, b0, et, p.mode, max_iter, 2);
         if (k) {
             p.lpr = 2;

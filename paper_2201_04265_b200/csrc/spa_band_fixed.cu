@@ -37,7 +37,9 @@ void *et_pair_nv(bool et, bool novote) {
 //   check-major; Table I 1032 (wc 9/6 VM+16-bit, 3 check-major).  Measured
 //   on B200 against NFIX = 0: C2 +2.6, C4 +2.9, C3-R3/4 +0.7, Table I R1/4
 //   (100k frames) +1.3 points of the SFU roofline; C3 (3,4) -0.7 (left out).
-// Lane-pair kernels (LPR = 2): Table I R1/4 and R1/2 in small batches.
+// Lane-pair kernels (LPR = 2): Table I R1/4 and R1/2 (wc x wr >= 64).  The
+// (3,12) codes measured worse with them (C3-R3/4 60 -> 47%, T1-R3/4 at 100k
+// frames 53 -> 51%), C1 -3%.
 template <int WR, int WC, int MODE, int N>
 void *lpr2(bool et, bool novote) {
     if (et) return reinterpret_cast<void *>(&band_kernel<WR, WC, 1, true, MODE, N, false, 0, false, 2>);
