@@ -105,55 +105,12 @@ __device__ __forceinline__ void psi_row(const float (&in)[D], float (&out)[D]) {
     for (int j = 0; j < D; ++j) out[j] = psi(in[j]);
 }
 
-// Saturation bound of a degree-D row: when every |L'_vc| of the row is >= it,
-// E'_cv = +-E_MAX for every edge, whichever psi tier would evaluate it: each
-// term is psi(y) = h0 2^-y (1 + O(2^-2y)) in every tier (relative excess
-// < 1e-25 at y >= 42), so every exclusive sum is <= (D-1) h0 2^-y_sat, and
-// its psi, >= C1 - lg2(sum) in every tier, is >= E_MAX + 0.02 -- a margin far
-// above the approx instructions' ~1e-6 error, so the clamp min(psi, E_MAX)
-// returns E_MAX bit for bit.  Reachable only below the input clamp: D <= 6
-// (y_sat = 43.205 for D = 6, 42.468 for D = 4; the clamp is 43.281).
+// Exclusive sums Phi_j = sum_{k != j} f_k of positive terms: never
+// total-minus-self (inf - inf, cancellation); a pairwise tree for D = 4, 6
+// (fewer adds, shorter chains; measured +1-2 points on C3/C4), prefix +
+// suffix otherwise (a tree for D = 12 measured -0.6 on C3-R3/4).
 template <int D>
-__host__ __device__ constexpr float sat_bound() {
-    // log2((D-1) h0) for D = 2..7 (h0 = 2.88539008 = 2 log2 e)
-    return D == 2 ? 40.863137f - 1.528766f + 1.528766f + 0.02f
-         : D == 3 ? 40.863137f - 1.528766f + 2.528766f + 0.02f
-         : D == 4 ? 40.863137f - 1.528766f + 3.113729f + 0.02f
-         : D == 5 ? 40.863137f - 1.528766f + 3.528766f + 0.02f
-         : D == 6 ? 40.863137f - 1.528766f + 3.850694f + 0.02f
-                  : 1e30f;
-}
-
-// Check-node update of one row (Eq. 5, readings Q2/Q3/Q7) in log2 units.
-// x[j] = L'_v - E'_cv (not yet clamped); e[j] <- new E'_cv.
-template <int D, bool VOTE>
-__device__ __forceinline__ void check_row(const float (&x)[D], float (&e)[D]) {
-    float f[D], ax[D];
-    uint32_t sx = (D & 1) ? 0x80000000u : 0u;     // (-1)^{d_c}
-#pragma unroll
-    for (int j = 0; j < D; ++j) {
-        sx ^= __float_as_uint(x[j]);
-        ax[j] = fminf(fabsf(x[j]), kClampB);
-    }
-    if constexpr (VOTE && sat_bound<D>() <= kClampB) {
-        // saturated rows (every input at the clamp: a converged frame under
-        // fixed iterations): E = +-E_MAX exactly as the full update gives it
-        float lo = ax[0];
-#pragma unroll
-        for (int j = 1; j < D; ++j) lo = fminf(lo, ax[j]);
-        if (__all_sync(__activemask(), lo >= sat_bound<D>())) {
-#pragma unroll
-            for (int j = 0; j < D; ++j)
-                e[j] = __uint_as_float(__float_as_uint(kEMaxB) | ((sx ^ __float_as_uint(x[j])) & 0x80000000u));
-            return;
-        }
-    }
-    psi_row<D, true, VOTE>(ax, f);
-    // exclusive sums Phi_j = sum_{k != j} f_k of positive terms: never
-    // total-minus-self (inf - inf, cancellation); a pairwise tree for D = 4, 6
-    // (fewer adds, shorter chains; measured +1-2 points on C3/C4), prefix +
-    // suffix otherwise (a tree for D = 12 measured -0.6 on C3-R3/4)
-    float ex[D];
+__device__ __forceinline__ void exclusive_sums(const float (&f)[D], float (&ex)[D]) {
     if constexpr (D == 6) {
         const float a01 = f[0] + f[1], a23 = f[2] + f[3], a45 = f[4] + f[5];
         const float o01 = a23 + a45, o23 = a01 + a45, o45 = a01 + a23;
@@ -178,6 +135,86 @@ __device__ __forceinline__ void check_row(const float (&x)[D], float (&e)[D]) {
             acc += f[j];
         }
     }
+}
+
+// Saturation bound of a degree-D row: when every |L'_vc| of the row is >= it,
+// E'_cv = +-E_MAX for every edge, whichever psi tier would evaluate it: each
+// term is psi(y) = h0 2^-y (1 + O(2^-2y)) in every tier (relative excess
+// < 1e-25 at y >= 42), so every exclusive sum is <= (D-1) h0 2^-y_sat, and
+// its psi, >= C1 - lg2(sum) in every tier, is >= E_MAX + 0.02 -- a margin far
+// above the approx instructions' ~1e-6 error, so the clamp min(psi, E_MAX)
+// returns E_MAX bit for bit.  Reachable only below the input clamp: D <= 6
+// (y_sat = 43.205 for D = 6, 42.468 for D = 4; the clamp is 43.281).
+template <int D>
+__host__ __device__ constexpr float sat_bound() {
+    // log2((D-1) h0) for D = 2..7 (h0 = 2.88539008 = 2 log2 e)
+    return D == 2 ? 40.863137f - 1.528766f + 1.528766f + 0.02f
+         : D == 3 ? 40.863137f - 1.528766f + 2.528766f + 0.02f
+         : D == 4 ? 40.863137f - 1.528766f + 3.113729f + 0.02f
+         : D == 5 ? 40.863137f - 1.528766f + 3.528766f + 0.02f
+         : D == 6 ? 40.863137f - 1.528766f + 3.850694f + 0.02f
+                  : 1e30f;
+}
+
+// Check-node update of one row (Eq. 5, readings Q2/Q3/Q7) in log2 units.
+// x[j] = L'_v - E'_cv (not yet clamped); e[j] <- new E'_cv.
+// Rows too wide to saturate (sat_bound > clamp, D >= 7) still reach a fixed
+// output once every input sits at the clamp: with the whole warp there, the
+// votes take the deep tiers, and E_j = +-M_j with M_j a constant of the
+// kernel -- clamp_row_mags computes it once per CTA through the very same
+// code (psi_row deep tiers, exclusive_sums), so the shortcut is bit-exact.
+template <int D>
+__device__ __forceinline__ void clamp_row_mags(float (&m)[D]) {
+    float ax[D], f[D], ex[D], g[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) ax[j] = kClampB;
+    psi_row<D, true, true>(ax, f);
+    exclusive_sums<D>(f, ex);
+    psi_row<D, false, true>(ex, g);
+#pragma unroll
+    for (int j = 0; j < D; ++j) m[j] = fminf(g[j], kEMaxB);
+}
+template <int D>
+__host__ __device__ constexpr bool has_clamp_tier() { return sat_bound<D>() > kClampB; }
+
+// cm: the row's clamp magnitudes (clamp_row_mags, shared memory; used when
+// has_clamp_tier<D>() and VOTE; may be null otherwise).
+template <int D, bool VOTE>
+__device__ __forceinline__ void check_row(const float (&x)[D], float (&e)[D], const float *cm = nullptr) {
+    float f[D], ax[D];
+    uint32_t sx = (D & 1) ? 0x80000000u : 0u;     // (-1)^{d_c}
+#pragma unroll
+    for (int j = 0; j < D; ++j) {
+        sx ^= __float_as_uint(x[j]);
+        ax[j] = fminf(fabsf(x[j]), kClampB);
+    }
+    if constexpr (VOTE && sat_bound<D>() <= kClampB) {
+        // saturated rows (every input at the clamp: a converged frame under
+        // fixed iterations): E = +-E_MAX exactly as the full update gives it
+        float lo = ax[0];
+#pragma unroll
+        for (int j = 1; j < D; ++j) lo = fminf(lo, ax[j]);
+        if (__all_sync(__activemask(), lo >= sat_bound<D>())) {
+#pragma unroll
+            for (int j = 0; j < D; ++j)
+                e[j] = __uint_as_float(__float_as_uint(kEMaxB) | ((sx ^ __float_as_uint(x[j])) & 0x80000000u));
+            return;
+        }
+    }
+    if constexpr (VOTE && has_clamp_tier<D>()) {
+        float lo = ax[0];
+#pragma unroll
+        for (int j = 1; j < D; ++j) lo = fminf(lo, ax[j]);
+        if (cm && __all_sync(__activemask(), lo >= kClampB)) {
+#pragma unroll
+            for (int j = 0; j < D; ++j)
+                e[j] = __uint_as_float(__float_as_uint(cm[j]) | ((sx ^ __float_as_uint(x[j])) & 0x80000000u));
+            return;
+        }
+    }
+    psi_row<D, true, VOTE>(ax, f);
+    float ex[D];
+    exclusive_sums<D>(f, ex);
     float g[D];
     psi_row<D, false, VOTE>(ex, g);
 #pragma unroll
@@ -278,9 +315,10 @@ __device__ __forceinline__ void check_row_pair(const float (&x)[D / 2], float (&
 
 // One row's update by one lane (LPR = 1) or a lane pair (LPR = 2).
 template <int D, bool VOTE, int LPR>
-__device__ __forceinline__ void check_any(const float (&x)[D / LPR], float (&e)[D / LPR], int h, unsigned pm) {
+__device__ __forceinline__ void check_any(const float (&x)[D / LPR], float (&e)[D / LPR], int h, unsigned pm,
+                                          const float *cm = nullptr) {
     if constexpr (LPR == 1) {
-        check_row<D, VOTE>(x, e);
+        check_row<D, VOTE>(x, e, cm);
     } else {
         check_row_pair<D, VOTE>(x, e, h, pm);
     }

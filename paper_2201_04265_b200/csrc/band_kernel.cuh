@@ -88,6 +88,22 @@ __global__ void __launch_bounds__(WC > 3 ? 256 * LPR : 1024, 1) band_kernel(cons
     const int32_t *lidx = code.band_lidx;
     const int32_t *vpos = code.band_vpos;
 
+    // rows too wide to saturate: the clamp tier's constant magnitudes
+    // (band_common.cuh clamp_row_mags), computed once per CTA by warp 0 and
+    // ordered before use by the frame loop's first barrier
+    constexpr bool CMT = has_clamp_tier<WR>() && !ET && !NOVOTE && LPR == 1;
+    __shared__ float s_cm[CMT ? WR : 1];
+    if constexpr (CMT) {
+        if (tt < 32) {
+            float m[WR];
+            clamp_row_mags<WR>(m);
+            if (tt == 0)
+#pragma unroll
+                for (int j = 0; j < WR; ++j) s_cm[j] = m[j];
+        }
+    }
+    const float *cmp = CMT ? s_cm : nullptr;
+
     unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};       // GEN: this CTA's counters (thread 0)
     __shared__ int s_err[2];
     for (;;) {
@@ -152,7 +168,7 @@ __global__ void __launch_bounds__(WC > 3 ? 256 * LPR : 1024, 1) band_kernel(cons
                 if (act) {
                     float x[WH];
                     lds_row<WH>(smem, lbase + (uint32_t(r) * WR + hoff) * 4u, x);
-                    check_any<WR, !ET && !NOVOTE, LPR>(x, e0[k], h, pm);
+                    check_any<WR, !ET && !NOVOTE, LPR>(x, e0[k], h, pm, cmp);
                 }
             }
         }
@@ -175,7 +191,7 @@ __global__ void __launch_bounds__(WC > 3 ? 256 * LPR : 1024, 1) band_kernel(cons
                     }
                     if (ET && LPR > 1) rp ^= __shfl_xor_sync(pm, rp, 1);
                     synd |= rp;
-                    check_any<WR, !ET && !NOVOTE, LPR>(x, e0[k], h, pm);
+                    check_any<WR, !ET && !NOVOTE, LPR>(x, e0[k], h, pm, cmp);
                 }
             }
 #pragma unroll
@@ -219,7 +235,7 @@ __global__ void __launch_bounds__(WC > 3 ? 256 * LPR : 1024, 1) band_kernel(cons
                     }
                     if (ET && LPR > 1) rp ^= __shfl_xor_sync(pm, rp, 1);
                     synd |= rp;
-                    check_any<WR, !ET && !NOVOTE, LPR>(x, e, h, pm);
+                    check_any<WR, !ET && !NOVOTE, LPR>(x, e, h, pm, cmp);
                     if (VM) {
 #pragma unroll
                         for (int j = 0; j < WH; ++j) *reinterpret_cast<float *>(smem + li[j] + delta) = e[j];
@@ -300,7 +316,7 @@ __global__ void __launch_bounds__(WC > 3 ? 256 * LPR : 1024, 1) band_kernel(cons
                             float x[WH];
 #pragma unroll
                             for (int j = 0; j < WH; ++j) x[j] = lv[j] - e0[k][j];
-                            check_any<WR, !ET && !NOVOTE, LPR>(x, e0[k], h, pm);
+                            check_any<WR, !ET && !NOVOTE, LPR>(x, e0[k], h, pm, cmp);
                         }
                     }
                 }

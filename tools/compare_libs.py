@@ -18,7 +18,8 @@ import ldpc_workloads as W  # noqa: E402
 # (config, frames, iterations, early termination, variant)
 CASES = [("C4", 1024, 50, False, 0), ("C3-R1/4", 1000, 50, False, 0), ("C3-R1/2", 1000, 50, False, 0),
          ("C2", 2000, 50, True, 0), ("C1", 2000, 30, False, 0), ("C5", 32, 50, False, 7),
-         ("C5", 8, 50, False, 5), ("C4", 2, 50, False, 7)]
+         ("C5", 8, 50, False, 5), ("C4", 2, 50, False, 7), ("C3-R3/4", 1000, 50, False, 0),
+         ("T1-R3/4", 2000, 30, False, 0), ("T1-R1/2", 500, 30, False, 0)]
 
 
 def run(lib_path, out):
