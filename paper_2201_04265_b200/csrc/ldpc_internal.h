@@ -132,8 +132,8 @@ inline size_t xband_smem_bytes(int32_t n, int32_t wc, int32_t wr, int32_t C, int
 // Cluster size of a code's exchange view.  Frames larger than one SM: the
 // smallest power of two C <= 16 with mb % C == 0 whose shared memory fits one
 // CTA and whose expected region fits 16-bit byte slots (throughput: C5 -> 8).
-// Frames that fit one SM: the largest C in {8, 4, 2} with >= 64 rows per CTA
-// (latency: stream mode and small batches, C4 -> 4).  0: no view.
+// Frames that fit one SM: the C of least modelled stream latency (below)
+// (latency: stream mode and small batches, C4 -> 9, C3 -> 6).  0: no view.
 inline bool xband_fits(int32_t n, int32_t wc, int32_t wr, int C) {
     if ((n / wr) % C) return false;
     if (xband_capacity_bound(n, wc, wr, C, 3) > kXbandMaxCapacity) return false;
@@ -163,9 +163,22 @@ inline int xband_cluster_size(int32_t n, int32_t wc, int32_t wr) {
         return (C >= 2 && C <= 16 && xband_fits(n, wc, wr, C)) ? C : 0;
     }
     if (band_frame_fits_sm(n, wc)) {
-        for (int C = 8; C >= 2; C /= 2)
-            if ((n / wr) % C == 0 && n / wr / C >= 64 && xband_fits(n, wc, wr, C)) return C;
-        return 0;
+        // latency view: the C dividing the band rows (<= 16, >= 32 rows per
+        // CTA) minimising 0.32 us x rows per CTA + 10.4 us x C -- the stream-
+        // mode latency model fitted on B200 (C4: C = 4 190 us, 6 145, 9 128,
+        // 12 135, 15 145; C3 R1/2: C = 2 103 us, 3 87, 6 84, 9 98)
+        const int32_t mb = n / wr;
+        int best = 0;
+        double best_cost = 1e30;
+        for (int C : {2, 3, 4, 5, 6, 8, 9, 10, 12, 15, 16}) {      // instantiated sizes
+            if (mb % C || mb / C < 32 || !xband_fits(n, wc, wr, C)) continue;
+            const double cost = 0.32 * (mb / C) + 10.4 * C;
+            if (cost < best_cost) {
+                best_cost = cost;
+                best = C;
+            }
+        }
+        return best;
     }
     if (!std::getenv("LDPC_XBAND_1SLOT") && xband2_fits(n, wc, wr) && xband_fits(n, wc, wr, 16)) return 16;
     for (int C = 2; C <= 16; C *= 2)

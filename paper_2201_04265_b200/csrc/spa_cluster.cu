@@ -715,6 +715,19 @@ void *pick_x_c(int C) {
         case 8: return reinterpret_cast<void *>(&xband_kernel<WR, 3, H, 8, MAXT>);
         case 16: return reinterpret_cast<void *>(&xband_kernel<WR, 3, H, 16, MAXT>);
     }
+    // latency views of frames that fit one SM: any C dividing the band rows
+    // (C4: mb = 2700 = 2^2 3^3 5^2, C3: mb = 666 = 2 3^2 37), one row per thread
+    if constexpr (H == 1) {
+        switch (C) {
+            case 3: return reinterpret_cast<void *>(&xband_kernel<WR, 3, 1, 3, MAXT>);
+            case 5: return reinterpret_cast<void *>(&xband_kernel<WR, 3, 1, 5, MAXT>);
+            case 6: return reinterpret_cast<void *>(&xband_kernel<WR, 3, 1, 6, MAXT>);
+            case 9: return reinterpret_cast<void *>(&xband_kernel<WR, 3, 1, 9, MAXT>);
+            case 10: return reinterpret_cast<void *>(&xband_kernel<WR, 3, 1, 10, MAXT>);
+            case 12: return reinterpret_cast<void *>(&xband_kernel<WR, 3, 1, 12, MAXT>);
+            case 15: return reinterpret_cast<void *>(&xband_kernel<WR, 3, 1, 15, MAXT>);
+        }
+    }
     return nullptr;
 }
 

@@ -525,7 +525,10 @@ ldpc_status resolve(const ldpc_code &c, int64_t frames, const ldpc_decode_opts &
         // rounds of the one-SM-per-frame kernel vs rounds of C-SM clusters, a
         // cluster round costing ~2/C of a band round (measured per-SM rate of
         // the exchange kernel is about half the band kernel's)
-        if (x_ok) {
+        // (only while the band kernel leaves SMs idle, frames <= SMs: small
+        // latency-view CTAs co-reside many per SM, which this cost model
+        // does not price)
+        if (x_ok && frames <= sms) {
             const int64_t rb = (frames + r.band.capacity - 1) / r.band.capacity;
             const int64_t rx = (frames + r.x.capacity - 1) / r.x.capacity;
             if (rx * 2 < rb * r.x.cluster) {
