@@ -58,9 +58,18 @@ __device__ __forceinline__ bool cta_sync_or(bool p) { return __syncthreads_or(p 
 // serial chain, for batches too small to fill the GPU one thread per row
 // (C1, Table I at 1000 frames).  Without psi votes the results are bit for
 // bit those of LPR = 1.  NFIX kernels only.
+// Launch bounds: the lane-pair kernels (NFIX) declare their exact block size
+// and BAND_LPR2_MINB blocks per SM (Table I wc = 9: 5 fit shared memory).
+#ifndef BAND_LPR2_MINB
+#define BAND_LPR2_MINB 5
+#endif
+constexpr int band_lb_threads(int wr, int wc, int b0, int nfix, int lpr) {
+    return lpr == 2 ? ((nfix / wr + b0 - 1) / b0 + 31) / 32 * 32 * 2 : (wc > 3 ? 256 : 1024);
+}
 template <int WR, int WC, int B0, bool ET, int MODE, int NFIX = 0, bool GEN = false, int RPRE = 0, bool NOVOTE = false,
           int LPR = 1>
-__global__ void __launch_bounds__(WC > 3 ? 256 * LPR : 1024, 1) band_kernel(const BandArgs a) {
+__global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), LPR == 2 ? BAND_LPR2_MINB : 1)
+    band_kernel(const BandArgs a) {
     // measured on B200: +1.1 points on C4 (MODE 2), +0.8..1.3 on wr = 12 codes,
     // -2..3 on check-major wr = 4 / 6 codes (C3 R1/4, R1/2)
     constexpr bool FUSE0 = BAND_FUSE0 && (MODE == 2 || WR >= 12 || NOVOTE);
