@@ -47,6 +47,12 @@ void *lpr2(bool et, bool novote) {
     return reinterpret_cast<void *>(&band_kernel<WR, WC, 1, false, MODE, N, false, 0, false, 2>);
 }
 
+// Rows per thread of a compile-time-n kernel when it differs from band_plan's
+// default (0: the default).  C3-R1/4 (999 rows per band): two rows per thread,
+// 512 threads, three CTAs per SM (its launch bounds) -- one 1024-thread CTA
+// held 64 registers per thread and left two thirds of shared memory idle.
+int band_fixed_b0(int n, int wr, int wc) { return (n == 3996 && wr == 4 && wc == 3) ? 2 : 0; }
+
 void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode, int max_iter, int lpr) {
     const bool novote = band_novote(n, wr, wc, max_iter, et);
     if (lpr == 2) {
@@ -72,6 +78,7 @@ void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode, i
     }
     if (wc == 3 && wr == 6 && n == 1008 && b0 == 1 && mode == 0) return et_pair<6, 3, 1, 0, 1008>(et);
     if (wc == 3 && wr == 6 && n == 96 && b0 == 1 && mode == 0) return et_pair_nv<6, 3, 1, 0, 96>(et, novote);   // C1
+    if (wc == 3 && wr == 4 && n == 3996 && b0 == 2 && mode == 0) return et_pair<4, 3, 2, 0, 3996>(et);   // C3-R1/4
     if (wc == 3 && n == 3996 && b0 == 1 && mode == 0) {
         if (wr == 6) return et_pair<6, 3, 1, 0, 3996>(et);
         if (wr == 12) return et_pair<12, 3, 1, 0, 3996>(et);
