@@ -250,6 +250,7 @@ bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPla
 // lpr: lanes per check row (1, or 2 for the lane-pair instantiations).
 void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode, int max_iter, int lpr = 1);
 int band_fixed_b0(int n, int wr, int wc);
+bool band_fixed_vm(int n, int wr, int wc);
 // Whether the band decoder runs without psi regime votes for this code and
 // iteration count (few-iteration configs with a compile-time-n kernel).
 inline bool band_novote(int n, int wr, int wc, int max_iter, bool et) {

@@ -377,7 +377,9 @@ bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPla
     p.r_in_smem = with_r + reserve <= size_t(optin);
     // Variable-major E (variant 4) drops the variable phase's index loads and
     // gathers; it pays off when the indices no longer fit in L1 (large n).
-    p.vm = variant == 4 || variant == 6 || (variant == 0 && (!p.r_in_smem || c.wc > 3));
+    p.vm = variant == 4 || variant == 6 ||
+           (variant == 0 && (!p.r_in_smem || c.wc > 3 ||
+                             (!std::getenv("LDPC_NO_NFIX") && band_fixed_vm(c.n, c.wr, c.wc))));
     // 16-bit offsets (variant 6, auto with VM when n <= 16383): +2% on C4
     p.mode = p.vm ? (((variant == 6 || variant == 0) && c.n <= 16383) ? 2 : 1) : 0;
     p.threads = ((mb + b0 - 1) / b0 + 31) / 32 * 32;

@@ -52,6 +52,13 @@ void *lpr2(bool et, bool novote) {
 // 512 threads, three CTAs per SM (its launch bounds) -- one 1024-thread CTA
 // held 64 registers per thread and left two thirds of shared memory idle.
 int band_fixed_b0(int n, int wr, int wc) { return (n == 3996 && wr == 4 && wc == 3) ? 2 : 0; }
+// Compile-time-n codes whose auto plan is variable-major E with 16-bit
+// offsets (MODE 2) although R fits shared memory: C3 (n = 3996).  Check-major
+// E left the variable phase gathering E at random banks (40% of its shared
+// wavefronts were conflicts once occupancy made the kernel MIO-bound).
+bool band_fixed_vm(int n, int wr, int wc) {
+    return n == 3996 && wc == 3 && (wr == 4 || wr == 6 || wr == 12) && !std::getenv("LDPC_NO_VM_FIXED");
+}
 
 void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode, int max_iter, int lpr) {
     const bool novote = band_novote(n, wr, wc, max_iter, et);
@@ -79,6 +86,11 @@ void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode, i
     if (wc == 3 && wr == 6 && n == 1008 && b0 == 1 && mode == 0) return et_pair<6, 3, 1, 0, 1008>(et);
     if (wc == 3 && wr == 6 && n == 96 && b0 == 1 && mode == 0) return et_pair_nv<6, 3, 1, 0, 96>(et, novote);   // C1
     if (wc == 3 && wr == 4 && n == 3996 && b0 == 2 && mode == 0) return et_pair<4, 3, 2, 0, 3996>(et);   // C3-R1/4
+    if (wc == 3 && n == 3996 && mode == 2) {      // C3, variable-major E + 16-bit offsets
+        if (wr == 4 && b0 == 2) return et_pair<4, 3, 2, 2, 3996>(et);
+        if (wr == 6 && b0 == 1) return et_pair<6, 3, 1, 2, 3996>(et);
+        if (wr == 12 && b0 == 1) return et_pair<12, 3, 1, 2, 3996>(et);
+    }
     if (wc == 3 && n == 3996 && b0 == 1 && mode == 0) {
         if (wr == 6) return et_pair<6, 3, 1, 0, 3996>(et);
         if (wr == 12) return et_pair<12, 3, 1, 0, 3996>(et);
