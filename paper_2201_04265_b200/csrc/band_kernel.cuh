@@ -81,8 +81,11 @@ constexpr int band_lb_threads(int wr, int wc, int b0, int nfix, int lpr) {
     return (lpr == 2 || band_lb_minb(wr, nfix, lpr) > 1) ? ((nfix / wr + b0 - 1) / b0 + 31) / 32 * 32 * lpr
                                                           : (wc > 3 ? 256 : 1024);
 }
+// LPR0: lanes per band-0 row (default LPR).  C1 runs one lane per row of
+// bands >= 1 (32 rows, all 32 lanes) and a lane pair per band-0 row (16 rows
+// on 32 lanes instead of 16), halving the variable phase's chain.
 template <int WR, int WC, int B0, bool ET, int MODE, int NFIX = 0, bool GEN = false, int RPRE = 0, bool NOVOTE = false,
-          int LPR = 1>
+          int LPR = 1, int LPR0 = LPR>
 __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_lb_minb(WR, NFIX, LPR))
     band_kernel(const BandArgs a) {
     // measured on B200: +1.1 points on C4 (MODE 2), +0.8..1.3 on wr = 12 codes,
@@ -102,6 +105,14 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
     const int T = NFIX ? TFIX * LPR : int(blockDim.x), tt = threadIdx.x, S = NFIX ? TFIX : a.row_stride;
     const int pr = tt / LPR, h = tt % LPR;   // row slot, half of the row
     const uint32_t hoff = uint32_t(h * WH);  // first element of this lane
+    // band-0 rows: LPR0 lanes each, row stride S0
+    constexpr int WH0 = WR / LPR0;
+    static_assert(LPR0 == LPR || (LPR == 1 && LPR0 == 2 && NFIX && !GEN && RPRE == 0 && WR % 2 == 0 &&
+                                  NFIX / WR <= TFIX * LPR / LPR0 * B0),
+                  "band-0 lane pairs: NFIX kernels whose band-0 rows fit the halved stride");
+    const int S0 = S * LPR / LPR0;
+    const int pr0 = tt / LPR0, h0 = tt % LPR0;
+    const uint32_t hoff0 = uint32_t(h0 * WH0);
     const bool r_in_smem = NFIX ? RFIX_SMEM : a.r_in_smem != 0;
     constexpr int NB = WC - 1;          // bands held in shared memory
     constexpr int B1 = NB * B0;         // max rows of bands >= 1 per thread
@@ -168,11 +179,11 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
         }
         for (int i = tt; i < (NB * n) >> 2; i += T)
             reinterpret_cast<float4 *>(smem)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        float e0[B0][WH];
+        float e0[B0][WH0];
 #pragma unroll
         for (int k = 0; k < B0; ++k)
 #pragma unroll
-            for (int j = 0; j < WH; ++j) e0[k][j] = 0.0f;
+            for (int j = 0; j < WH0; ++j) e0[k][j] = 0.0f;
         __syncthreads();
 
         int32_t iters = a.max_iter;
@@ -186,13 +197,13 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
         if constexpr (FUSE0) {
 #pragma unroll
             for (int k = 0; k < B0; ++k) {
-                const int r = pr + k * S;
-                const bool act = pr < S && r < mb;
-                const unsigned pm = LPR > 1 ? __ballot_sync(0xffffffffu, act) : 0u;
+                const int r = pr0 + k * S0;
+                const bool act = pr0 < S0 && r < mb;
+                const unsigned pm = LPR0 > 1 ? __ballot_sync(0xffffffffu, act) : 0u;
                 if (act) {
-                    float x[WH];
-                    lds_row<WH>(smem, lbase + (uint32_t(r) * WR + hoff) * 4u, x);
-                    check_any<WR, !ET && !NOVOTE, LPR>(x, e0[k], h, pm, cmp);
+                    float x[WH0];
+                    lds_row<WH0>(smem, lbase + (uint32_t(r) * WR + hoff0) * 4u, x);
+                    check_any<WR, !ET && !NOVOTE, LPR0>(x, e0[k], h0, pm, cmp);
                 }
             }
         }
@@ -201,21 +212,21 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
             uint32_t synd = FUSE0 ? synd0 : 0u;
 #pragma unroll
             for (int k = 0; k < (FUSE0 ? 0 : B0); ++k) {
-                const int r = pr + k * S;
-                const bool act = pr < S && r < mb;
-                const unsigned pm = LPR > 1 ? __ballot_sync(0xffffffffu, act) : 0u;
+                const int r = pr0 + k * S0;
+                const bool act = pr0 < S0 && r < mb;
+                const unsigned pm = LPR0 > 1 ? __ballot_sync(0xffffffffu, act) : 0u;
                 if (act) {
-                    float lv[WH], x[WH];
-                    lds_row<WH>(smem, lbase + (uint32_t(r) * WR + hoff) * 4u, lv);
+                    float lv[WH0], x[WH0];
+                    lds_row<WH0>(smem, lbase + (uint32_t(r) * WR + hoff0) * 4u, lv);
                     uint32_t rp = 0;      // this row's syndrome bit (Eq. 1)
 #pragma unroll
-                    for (int j = 0; j < WH; ++j) {
+                    for (int j = 0; j < WH0; ++j) {
                         x[j] = lv[j] - e0[k][j];
                         if (ET) rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
                     }
-                    if (ET && LPR > 1) rp ^= __shfl_xor_sync(pm, rp, 1);
+                    if (ET && LPR0 > 1) rp ^= __shfl_xor_sync(pm, rp, 1);
                     synd |= rp;
-                    check_any<WR, !ET && !NOVOTE, LPR>(x, e0[k], h, pm, cmp);
+                    check_any<WR, !ET && !NOVOTE, LPR0>(x, e0[k], h0, pm, cmp);
                 }
             }
 #pragma unroll
@@ -294,53 +305,53 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
             synd0 = 0;
 #pragma unroll
             for (int k = 0; k < B0; ++k) {
-                const int r = pr + k * S;
-                const bool act = pr < S && r < mb;
-                const unsigned pm = LPR > 1 ? __ballot_sync(0xffffffffu, act) : 0u;
+                const int r = pr0 + k * S0;
+                const bool act = pr0 < S0 && r < mb;
+                const unsigned pm = LPR0 > 1 ? __ballot_sync(0xffffffffu, act) : 0u;
                 if (act) {
-                    float rv[WH], lv[WH];
+                    float rv[WH0], lv[WH0];
                     if (k < RP && !r_in_smem) {
 #pragma unroll
-                        for (int j = 0; j < WH; ++j) rv[j] = rpre[k < RP ? k : 0][j];
+                        for (int j = 0; j < WH0; ++j) rv[j] = rpre[k < RP ? k : 0][j];
                     } else {
-                        lds_row<WH>(reinterpret_cast<const char *>(Rs), (uint32_t(r) * WR + hoff) * 4u, rv);
+                        lds_row<WH0>(reinterpret_cast<const char *>(Rs), (uint32_t(r) * WR + hoff0) * 4u, rv);
                     }
                     if (VM) {
                         // this row's variables are contiguous in every band's E_b
 #pragma unroll
-                        for (int j = 0; j < WH; ++j) lv[j] = rv[j] + e0[k][j];
+                        for (int j = 0; j < WH0; ++j) lv[j] = rv[j] + e0[k][j];
 #pragma unroll
                         for (int b = 0; b < NB; ++b) {
-                            float eb[WH];
-                            lds_row<WH>(smem, uint32_t(b) * n * 4u + (uint32_t(r) * WR + hoff) * 4u, eb);
+                            float eb[WH0];
+                            lds_row<WH0>(smem, uint32_t(b) * n * 4u + (uint32_t(r) * WR + hoff0) * 4u, eb);
 #pragma unroll
-                            for (int j = 0; j < WH; ++j) lv[j] += eb[j];
+                            for (int j = 0; j < WH0; ++j) lv[j] += eb[j];
                         }
                     } else {
-                        int32_t vp[WH * NB];
-                        ldg_idx<WH * NB>(vpos + (size_t(r) * WR + hoff) * NB, vp);
+                        int32_t vp[WH0 * NB];
+                        ldg_idx<WH0 * NB>(vpos + (size_t(r) * WR + hoff0) * NB, vp);
 #pragma unroll
-                        for (int j = 0; j < WH; ++j) {
+                        for (int j = 0; j < WH0; ++j) {
                             float s = rv[j] + e0[k][j];
 #pragma unroll
                             for (int b = 0; b < NB; ++b) s += *reinterpret_cast<const float *>(smem + vp[j * NB + b]);
                             lv[j] = s;
                         }
                     }
-                    sts_row<WH>(smem, lbase + (uint32_t(r) * WR + hoff) * 4u, lv);
+                    sts_row<WH0>(smem, lbase + (uint32_t(r) * WR + hoff0) * 4u, lv);
                     if constexpr (FUSE0) {
                         if (ET) {
                             uint32_t rp = 0;      // this band-0 row's syndrome bit of z^t (Eq. 1)
 #pragma unroll
-                            for (int j = 0; j < WH; ++j) rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
-                            if (LPR > 1) rp ^= __shfl_xor_sync(pm, rp, 1);
+                            for (int j = 0; j < WH0; ++j) rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
+                            if (LPR0 > 1) rp ^= __shfl_xor_sync(pm, rp, 1);
                             synd0 |= rp;
                         }
                         if (t < a.max_iter) {
-                            float x[WH];
+                            float x[WH0];
 #pragma unroll
-                            for (int j = 0; j < WH; ++j) x[j] = lv[j] - e0[k][j];
-                            check_any<WR, !ET && !NOVOTE, LPR>(x, e0[k], h, pm, cmp);
+                            for (int j = 0; j < WH0; ++j) x[j] = lv[j] - e0[k][j];
+                            check_any<WR, !ET && !NOVOTE, LPR0>(x, e0[k], h0, pm, cmp);
                         }
                     }
                 }

@@ -84,7 +84,12 @@ void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode, i
         return et_pair<6, 3, 3, 2, 16200>(et);
     }
     if (wc == 3 && wr == 6 && n == 1008 && b0 == 1 && mode == 0) return et_pair<6, 3, 1, 0, 1008>(et);
-    if (wc == 3 && wr == 6 && n == 96 && b0 == 1 && mode == 0) return et_pair_nv<6, 3, 1, 0, 96>(et, novote);   // C1
+    if (wc == 3 && wr == 6 && n == 96 && b0 == 1 && mode == 0) {     // C1: band-0 rows on lane pairs
+        if (std::getenv("LDPC_NO_B0PAIR")) return et_pair_nv<6, 3, 1, 0, 96>(et, novote);
+        if (et) return reinterpret_cast<void *>(&band_kernel<6, 3, 1, true, 0, 96, false, 0, false, 1, 2>);
+        if (novote) return reinterpret_cast<void *>(&band_kernel<6, 3, 1, false, 0, 96, false, 0, true, 1, 2>);
+        return reinterpret_cast<void *>(&band_kernel<6, 3, 1, false, 0, 96, false, 0, false, 1, 2>);
+    }
     if (wc == 3 && wr == 4 && n == 3996 && b0 == 2 && mode == 0) return et_pair<4, 3, 2, 0, 3996>(et);   // C3-R1/4
     if (wc == 3 && n == 3996 && mode == 2) {      // C3, variable-major E + 16-bit offsets
         if (wr == 4 && b0 == 2) return et_pair<4, 3, 2, 2, 3996>(et);
