@@ -5,14 +5,18 @@ count (+ NCCL all-reduce of the counters when N > 1) on B200.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--config C4] [--frames F]
 
-One step = one pass of every §8(a) row over one batch of synthetic frames
-resident in HBM: ldpc_encode (e1) -> ldpc_decode (a1-a8) -> ldpc_count_errors
-(a9) -> all_reduce(int64[6]) (a9, N > 1).  Default workload: BASELINE.json
-configs[3] (C4: n = 16200 (3,6), 200,000 frames, 50 fixed iterations,
-Eb/N0 1.5 dB, with the bit-packed encode of all frames) -- the largest config
-that fits one GPU (C5's 1,000,000 frames of n = 64800 need 259 GB of LLRs).
-Frames shard across ranks by Eq. 9 (weak scaling: every rank decodes its own
-batch; frame indices are global so results do not depend on N).
+One step = one pass of every §8(a) row over the step's synthetic frames:
+ldpc_encode (e1) -> ldpc_decode (a1-a8) -> ldpc_count_errors (a9) ->
+all_reduce(int64[6]) (a9, N > 1).  Default workload: BASELINE.json configs[3]
+(C4: n = 16200 (3,6), 200,000 frames, 50 fixed iterations, Eb/N0 1.5 dB, with
+the bit-packed encode of all frames) -- the largest config whose LLRs fit one
+GPU, resident in HBM.  The step's frames are split across ranks by Eq. 9
+(strong scaling, the default: the config's frame count is fixed as
+N grows); `--scaling weak` gives every rank a batch of its own.  Frame indices
+are global, so results do not depend on N.  `--config C5` runs the 10^6
+frames of configs[4] in 16,384-frame chunks per rank (their LLRs, 259 GB, do
+not fit), each chunk encode -> channel -> decode -> count.  `--config C2`
+sweeps its five Eb/N0 points.
 
 Rank 0 prints one JSON line.  `--impl reference` times the CPU oracle on the
 host cores (the reference arm for this paper-only tier).
@@ -37,6 +41,7 @@ import ldpc_workloads as W  # noqa: E402
 # edge per iteration, ex2 + lg2 each), 16 MUFU/clk/SM, 148 SMs.
 MUFU_PER_CLK_PER_SM = 16
 MUFU_PER_EDGE_UPDATE = 4
+E2E_PINNED_BYTES = 16e9          # pinned host memory for the e2e arm, over all ranks
 KERNEL_NAMES = {1: "spa_decode_kernel (generic, on-chip)", 2: "spa_decode_kernel (generic, global state)",
                 3: "band_kernel (check-major E)", 4: "band_kernel (variable-major E)",
                 5: "band_cluster_kernel (L2 gathers)", 6: "band_kernel (variable-major E, 16-bit offsets)",
@@ -51,7 +56,13 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C4", choices=sorted(W.ALL))
-    ap.add_argument("--frames", type=int, default=0, help="override frames per GPU per step")
+    ap.add_argument("--frames", type=int, default=0,
+                    help="override the step's frames (strong: total over ranks; weak: per rank)")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="strong: the step's frames are split across ranks by Eq. 9 (default); "
+                         "weak: every rank decodes a batch of its own")
+    ap.add_argument("--chunk", type=int, default=16384,
+                    help="frames per launch when a rank's LLRs exceed the 40 GB HBM budget (C5)")
     ap.add_argument("--e2e-frames", type=int, default=0, help="cap on e2e frames per step (0 = the batch)")
     ap.add_argument("--e2e-chunk", type=int, default=8192, help="frames per H2D/compute/D2H pipeline chunk (e2e)")
     ap.add_argument("--early-term", type=int, choices=[0, 1], default=None,
@@ -102,8 +113,8 @@ def run_stream(args):
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=s):
         serial()
-    it.zero_()
     with torch.cuda.stream(s):              # graph replays on the current stream
+        it.zero_()                          # ordered before the replays on the same stream
         for _ in range(args.warmup):
             g.replay()
     torch.cuda.synchronize()
@@ -311,10 +322,11 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "decoded info Gbit/s", "value": value, "unit": "Gbit/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "long double (x87 f80)",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "long double (x87 f80)",
         "data": "synthetic (seeded Philox frames, BASELINE.json recipe)",
-        # same config as our arm; each timed step is the bounded sample in cpu_baseline.sample
-        "config": workload_config(wl, args.frames or wl.frames, args.gpus),
+        # our arm's workload; each timed step decodes the bounded sample named in cpu_baseline.sample
+        "config": dict(workload_config(wl, F, args.gpus, scaling=args.scaling, total=F),
+                       reference_sample=sample),
         "cpu_baseline": {"value": value, "unit": "Gbit/s", "cores": threads, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": "Gbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -337,18 +349,272 @@ def dram_traffic(wl, frames):
     return None
 
 
-def workload_config(wl, frames, gpus, l2_policy=None, launch=None):
+def issue_profile(wl):
+    """Warp instructions executed per edge-update of the decode kernel, from
+    the committed ncu capture of this workload (profiles/issue.json); None if
+    there is none."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "issue.json")) as f:
+            return json.load(f).get(wl.name)
+    except Exception:
+        return None
+
+
+def roofline(wl, variant, achieved, sms, clock_mhz, frames):
+    """The decode kernel's roofline.  SFU model: 4 MUFU per
+    edge-update (2 phi per edge and iteration, ex2 + lg2 each) at 16 MUFU/clk/SM.
+    Issue model: thread-instructions per edge-update (ncu) x edge-updates/s
+    against 148 SMs x 4 schedulers x 32 lanes per clock.  The SFU model is the
+    primary bound unless exact shortcuts (saturation / deep tiers) make the
+    kernel beat it (fraction > 1): then the price no longer binds and the
+    issue model is primary."""
+    peak = sms * MUFU_PER_CLK_PER_SM * clock_mhz * 1e6 / MUFU_PER_EDGE_UPDATE / 1e9
+    sfu = {"bound": "alu", "kernel": f"ldpc_decode variant {variant}: {KERNEL_NAMES.get(variant, '?')}",
+           "achieved": achieved, "peak": peak, "unit": "Gedge-updates/s", "frac": achieved / peak,
+           "traffic": dram_traffic(wl, frames),
+           "peak_basis": f"SFU: {sms} SMs x 16 MUFU/clk x {clock_mhz:.0f} MHz / 4 MUFU per edge-update (DESIGN.md)"}
+    prof = issue_profile(wl)
+    if not prof:
+        return sfu
+    ipe = float(prof["thread_instructions_per_edge_update"])
+    issue_peak = sms * 4 * 32 * clock_mhz * 1e6 / 1e12                     # T thread-instr/s
+    issue = {"bound": "issue", "achieved": achieved * 1e9 * ipe / 1e12, "peak": issue_peak,
+             "unit": "Tthread-instr/s", "frac": achieved * 1e9 * ipe / 1e12 / issue_peak,
+             "thread_instructions_per_edge_update": ipe, "budget_at_100pct": 32.0,
+             "source": prof.get("source", "profiles/issue.json")}
+    if sfu["frac"] > 1.0:
+        out = dict(issue, kernel=sfu["kernel"], traffic=sfu["traffic"],
+                   peak_basis=f"issue: {sms} SMs x 4 schedulers x 32 lanes x {clock_mhz:.0f} MHz; "
+                              "thread-instructions per edge-update from ncu (the SFU price is beaten by exact "
+                              "shortcuts, so it no longer binds)")
+        out["sfu_model"] = {k: sfu[k] for k in ("achieved", "peak", "unit", "frac")}
+        return out
+    sfu["issue_model"] = {k: issue[k] for k in ("achieved", "peak", "unit", "frac",
+                                                "thread_instructions_per_edge_update", "source")}
+    return sfu
+
+
+def workload_config(wl, frames, gpus, l2_policy=None, launch=None, scaling="strong", total=None, point=0,
+                    chunk=None):
+    total = total if total is not None else wl.frames
+    par = (f"dp{gpus}: {total} frames per step split across ranks by Eq. 9 (strong scaling)" if scaling == "strong"
+           else f"dp{gpus}: every rank decodes its own {frames}-frame batch (weak scaling)")
     return {"workload": f"{wl.name}: Gallager ({wl.wc},{wl.wr}) n={wl.n}, {wl.frames} frames in BASELINE.json, "
                         f"{wl.max_iter} {'max (early term.)' if wl.early_term else 'fixed'} SPA iterations, "
-                        f"BPSK/AWGN Eb/N0={wl.ebn0_db[0]} dB, fp32 LLRs",
-            "n": wl.n, "wc": wl.wc, "wr": wl.wr, "frames_per_gpu_per_step": frames, "iterations": wl.max_iter,
-            "early_term": wl.early_term, "ebn0_db": wl.ebn0_db[0], "sigma": wl.sigma(), "code_seed": W.CODE_SEED,
-            "frame_seed": wl.frame_seeds[0], "parallelism": f"dp{gpus} (frames sharded by Eq. 9, weak scaling)",
+                        f"BPSK/AWGN Eb/N0={wl.ebn0_db[point]} dB, fp32 LLRs",
+            "n": wl.n, "wc": wl.wc, "wr": wl.wr, "frames_per_step": total if scaling == "strong" else frames * gpus,
+            "frames_per_gpu_per_step": frames, "iterations": wl.max_iter,
+            "early_term": wl.early_term, "ebn0_db": wl.ebn0_db[point], "sigma": wl.sigma(point),
+            "code_seed": W.CODE_SEED, "frame_seed": wl.frame_seeds[point], "parallelism": par,
             "l2_policy": l2_policy or "inputs larger than L2 (LLR batch >> 126 MB), no flush needed",
+            **({"chunk_frames": chunk} if chunk else {}),
             **({"launch": launch} if launch else {})}
 
 
 # --------------------------------------------------------------------------- our arm
+def rank_share(total: int, rank: int, world: int, scaling: str):
+    """(frame0, count) of this rank.  Strong scaling: the Eq. 9 block of the
+    step's `total` frames (dist.shard); weak: a batch of `total`
+    frames of its own at global indices rank*total.  Frame f depends only on
+    (seed, f), so the frames -- and the summed counters -- do not depend on N."""
+    from paper_2201_04265_b200 import dist as LD
+    if scaling == "strong":
+        return LD.shard(total, rank, world)
+    return LD.weak_shard(total, rank)
+
+
+def chunk_spans(frame0: int, count: int, chunk: int):
+    """Contiguous launches [(f0, m)] covering [frame0, frame0 + count)."""
+    return [(frame0 + a, min(chunk, count - a)) for a in range(0, count, max(chunk, 1))]
+
+
+def reduce_step(counters=None, times=None):
+    """The only collectives: all_reduce(SUM) of the int64[6] counters (inside
+    every timed step) and all_reduce(MAX) of the ranks' device times (after
+    the timed region); no-ops on one process."""
+    from paper_2201_04265_b200 import dist as LD
+    if counters is not None:
+        LD.all_reduce_counters(counters)
+    if times is not None:
+        LD.max_over_ranks(times)
+    return counters, times
+
+
+class RankWork:
+    """One rank's share of a step on the device.
+
+    resident (the share's LLRs fit the HBM budget, e.g. C4): info bits,
+      codewords and LLRs are generated once (untimed); a step is encode (e1)
+      -> decode (a1-a8) -> count (a9) over the whole share.
+    chunked (C5: 10^6 frames x 259 KB of LLRs): the share's info bits are
+      resident; a step runs, per chunk of `chunk` frames, encode -> channel
+      (BPSK/AWGN LLRs of the chunk, Eq. 4; kept inside the timed region, ~0.2%
+      of a chunk) -> decode -> count, all on one stream."""
+
+    def __init__(self, L, code, wl, point, frame0, count, chunk, dev, variant, budget_bytes=40e9):
+        import torch
+        self.L, self.code, self.wl, self.variant = L, code, wl, variant
+        info = code.info
+        self.n, self.k = info.n, info.k
+        kw, nw = L.words(self.k), L.words(self.n)
+        self.frame0, self.count = frame0, count
+        self.resident = count * self.n * 4 <= budget_bytes
+        self.spans = [(frame0, count)] if self.resident else chunk_spans(frame0, count, chunk)
+        Fb = max(count if self.resident else min(chunk, count), 1)
+        self.Fb = Fb
+        self.seed, self.sigma = wl.frame_seeds[point], wl.sigma(point)
+        self.d_info = torch.empty((max(count, 1), kw), dtype=torch.int32, device=dev)
+        self.d_cw = torch.empty((Fb, nw), dtype=torch.int32, device=dev)
+        self.d_llr = torch.empty((Fb, self.n), dtype=torch.float32, device=dev)
+        self.d_bits = torch.empty((Fb, nw), dtype=torch.int32, device=dev)
+        self.d_syn = torch.empty(Fb, dtype=torch.uint8, device=dev)
+        self.d_it = torch.empty(Fb, dtype=torch.int32, device=dev)
+        self.d_ctr = torch.zeros(6, dtype=torch.int64, device=dev)
+        wsb = L.ldpc_decode_workspace_bytes(code, Fb, wl.max_iter, wl.early_term, variant)
+        self.d_ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev) if wsb else None
+        self.ev = [(torch.cuda.Event(enable_timing=True, external=True),
+                    torch.cuda.Event(enable_timing=True, external=True)) for _ in self.spans]
+        if count:
+            L.ldpc_gen_info(self.seed, frame0, count, self.k, self.d_info)
+            if self.resident:
+                L.ldpc_encode(code, self.d_info, self.d_cw, count)
+                L.ldpc_channel(code, self.seed, frame0, count, self.d_cw, self.sigma, self.d_llr)
+
+    def device_work(self, s):
+        import torch
+        L, code, wl = self.L, self.code, self.wl
+        with torch.cuda.stream(s):
+            self.d_ctr.zero_()
+        for (f0, m), (e0, e1) in zip(self.spans, self.ev):
+            if m == 0:
+                continue
+            a = f0 - self.frame0
+            info = self.d_info[a:a + m]
+            L.ldpc_encode(code, info, self.d_cw, m, stream=s)
+            if not self.resident:
+                L.ldpc_channel(code, self.seed, f0, m, self.d_cw, self.sigma, self.d_llr, stream=s)
+            e0.record(s)
+            L.ldpc_decode(code, self.d_llr, m, self.d_bits, self.d_syn, self.d_it, None, self.d_ws, wl.max_iter,
+                          wl.early_term, self.variant, stream=s)
+            e1.record(s)
+            L.ldpc_count_errors(code, info, self.d_bits, self.d_cw, self.d_syn, self.d_it, m, self.d_ctr, stream=s)
+
+    def decode_ms(self):
+        return sum(e0.elapsed_time(e1) for (f0, m), (e0, e1) in zip(self.spans, self.ev) if m)
+
+
+def graph_kernel_launches(graph):
+    """Kernel nodes of a captured step that are this library's (not torch's
+    fill kernels): counted from the CUDA graph itself."""
+    try:
+        from cuda.bindings import runtime as rt
+        g = graph.raw_cuda_graph()
+        err, nodes, num = rt.cudaGraphGetNodes(g, 0)
+        err, nodes, num = rt.cudaGraphGetNodes(g, num)
+        ours = 0
+        for nd in nodes:
+            err, ty = rt.cudaGraphNodeGetType(nd)
+            if ty != rt.cudaGraphNodeType.cudaGraphNodeTypeKernel:
+                continue
+            err, prm = rt.cudaGraphKernelNodeGetParams(nd)
+            err, name = rt.cudaFuncGetName(prm.func)
+            name = name.decode() if isinstance(name, bytes) else str(name)
+            if "ldpc" in name:
+                ours += 1
+        return ours
+    except Exception:
+        return None
+
+
+def measure_point(args, L, code, wl, point, dev, rank, world, launched, sms, props):
+    """Time one Eb/N0 point of the workload: W warm-up steps, K timed steps
+    (barrier + synchronize on both sides, CUDA events on the launching stream,
+    max over ranks).  Returns the rank-0 result dict."""
+    import torch
+    import torch.distributed as dist
+
+    total = args.frames or wl.frames
+    frame0, count = rank_share(total, rank, world, args.scaling)
+    work = RankWork(L, code, wl, point, frame0, count, args.chunk, dev, args.variant)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    # The step's kernels are captured once in a CUDA graph and replayed, so host
+    # launch overhead stays out of the device timeline (it dominates small
+    # batches such as C1); the decode events are external event nodes.
+    work.device_work(stream)                  # plans resolved, attributes set before capture
+    torch.cuda.synchronize()
+    graph, launches = None, None
+    if not args.eager:
+        graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(graph, stream=cap):
+                work.device_work(cap)
+        torch.cuda.synchronize()
+        launches = graph_kernel_launches(graph)
+
+    def step():
+        if graph is not None:
+            graph.replay()
+        else:
+            work.device_work(stream)
+        if launched:
+            reduce_step(work.d_ctr)             # a9: the step's counters summed over ranks (NCCL)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # Batches smaller than twice the L2 are evicted before every step by
+    # writing a buffer four times the L2 size, outside the step's events;
+    # larger inputs stream through L2 on their own.
+    l2 = int(getattr(props, "L2_cache_size", 126 * 2**20) or 126 * 2**20)
+    in_bytes = count * work.n * 4
+    flush = torch.empty(l2, dtype=torch.int32, device=dev) if in_bytes < 2 * l2 else None
+    l2_policy = (f"LLR batch {in_bytes / 2**20:.1f} MiB < 2 x L2: L2 flushed before every timed step "
+                 f"({4 * l2 / 2**20:.0f} MiB write, untimed)" if flush is not None else None)
+    ctr_total = torch.zeros(6, dtype=torch.int64, device=dev)
+    if launched:
+        dist.barrier()
+    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    dec_ms = []
+    with ClockSampler(dev.index) as clk:
+        for i in range(args.steps):
+            if flush is not None:
+                flush.add_(1)                   # evict the previous step's inputs from L2 (untimed)
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+            ends[i].synchronize()
+            dec_ms.append(work.decode_ms())     # decode kernel time of this step
+            ctr_total.add_(work.d_ctr)
+        torch.cuda.synchronize()
+    if launched:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    t = torch.tensor([sum(step_ms), sum(dec_ms)], dtype=torch.float64, device=dev)
+    reduce_step(None, t)                        # max over ranks (counters were summed every step)
+    total_ms, dec_total_ms = float(t[0]), float(t[1])
+    ctr = (ctr_total.cpu().numpy() // max(args.steps, 1)).tolist()   # per step, all ranks
+    k = work.k
+    variant = L.ldpc_decode_variant(code, work.Fb, wl.max_iter, wl.early_term, args.variant)
+    clock_mhz = measured_peaks().get("sm_max_mhz", 1965.0)
+    # decode kernel throughput of the slowest rank, per GPU (its own edge-updates)
+    eu_rank = count * wl.edges * (ctr[4] / max(ctr[5], 1))
+    achieved = eu_rank / (dec_total_ms / args.steps / 1e3) / 1e9 if dec_total_ms > 0 else 0.0
+    res = {
+        "work": work, "graph": graph, "launches_per_step": launches, "count": count, "frame0": frame0,
+        "total_ms": total_ms, "dec_ms": dec_total_ms, "counters": ctr, "k": k, "variant": variant,
+        "value": ctr[5] * k * args.steps / (total_ms / 1e3) / 1e9,
+        "edge_updates_per_s": ctr[4] * wl.edges * args.steps / (total_ms / 1e3),
+        "roofline": roofline(wl, variant, achieved, sms, clock_mhz, work.Fb), "clocks": clk.summary(),
+        "l2_policy": l2_policy, "total": total,
+    }
+    return res
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -358,7 +624,6 @@ def main():
     if args.mode == "simulate":
         return run_simulate(args)
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -372,129 +637,24 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", torch.cuda.current_device())
     wl = workload(args)
-    frames = args.frames or (wl.frames if wl.frames * wl.n * 4 < 40e9 else 16384)
     props = torch.cuda.get_device_properties(dev)
     sms = props.multi_processor_count
 
-    # ---- setup (untimed): code, device image, frames
+    # ---- setup (untimed): code and device image
     t_setup = time.perf_counter()
     code = L.ldpc_make_H(wl.n, wl.wc, wl.wr, W.CODE_SEED)
     L.ldpc_make_G_device(code, dev)           # bit-identical to ldpc_make_G, ~15x faster (profiles/r01_make_G.jsonl)
     L.ldpc_code_bind_device(code, dev)
-    info = code.info
-    n, k = info.n, info.k
-    kw, nw = L.words(k), L.words(n)
-    frame0, _ = LD.weak_shard(frames, rank)   # global frame indices: rank r owns [r F, (r+1) F)
-    d_info = torch.empty((frames, kw), dtype=torch.int32, device=dev)
-    d_cw = torch.empty((frames, nw), dtype=torch.int32, device=dev)
-    d_llr = torch.empty((frames, n), dtype=torch.float32, device=dev)
-    d_bits = torch.empty((frames, nw), dtype=torch.int32, device=dev)
-    d_syn = torch.empty(frames, dtype=torch.uint8, device=dev)
-    d_it = torch.empty(frames, dtype=torch.int32, device=dev)
-    d_ctr = torch.zeros(6, dtype=torch.int64, device=dev)
-    wsb = L.ldpc_decode_workspace_bytes(code, frames, wl.max_iter, wl.early_term, args.variant)
-    d_ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev) if wsb else None
-    seed = wl.frame_seeds[0]
-    L.ldpc_gen_info(seed, frame0, frames, k, d_info)
-    L.ldpc_encode(code, d_info, d_cw, frames)
-    L.ldpc_channel(code, seed, frame0, frames, d_cw, wl.sigma(), d_llr)
-    torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
-    stream = torch.cuda.current_stream()
 
-    def device_work(s):
-        L.ldpc_encode(code, d_info, d_cw, frames, stream=s)
-        ev_d0.record(s)
-        L.ldpc_decode(code, d_llr, frames, d_bits, d_syn, d_it, None, d_ws, wl.max_iter, wl.early_term,
-                      args.variant, stream=s)
-        ev_d1.record(s)
-        if launched:
-            d_ctr.zero_()       # per-step counters for the all-reduce across ranks
-        L.ldpc_count_errors(code, d_info, d_bits, d_cw, d_syn, d_it, frames, d_ctr, stream=s)
-
-    # The step's kernels (encode -> decode -> count) are captured once in a
-    # CUDA graph and replayed, so host launch overhead stays out of the device
-    # timeline (it dominates small batches such as C1); the decode events are
-    # external event nodes of the graph.  --eager launches them one by one.
-    graph = None
-    ev_d0 = torch.cuda.Event(enable_timing=True, external=not args.eager)
-    ev_d1 = torch.cuda.Event(enable_timing=True, external=not args.eager)
-    device_work(stream)                       # plans resolved, attributes set before capture
-    torch.cuda.synchronize()
-    if not args.eager:
-        graph = torch.cuda.CUDAGraph()
-        cap = torch.cuda.Stream()
-        cap.wait_stream(stream)
-        with torch.cuda.stream(cap):
-            with torch.cuda.graph(graph, stream=cap):
-                device_work(cap)
-        torch.cuda.synchronize()
-
-    def step():
-        if graph is not None:
-            graph.replay()
-        else:
-            device_work(stream)
-        if launched:
-            LD.all_reduce_counters(d_ctr)
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-
-    # ---- timed region.  Batches smaller than twice the L2 are evicted before
-    # every step by writing a buffer four times the L2 size, outside the step's
-    # events; larger batches stream through L2 on their own.
-    l2 = int(getattr(props, "L2_cache_size", 126 * 2**20) or 126 * 2**20)
-    in_bytes = frames * n * 4
-    flush = torch.empty(4 * l2 // 4, dtype=torch.int32, device=dev) if in_bytes < 2 * l2 else None
-    l2_policy = (f"LLR batch {in_bytes / 2**20:.1f} MiB < 2 x L2: L2 flushed before every timed step "
-                 f"({4 * l2 / 2**20:.0f} MiB write, untimed)" if flush is not None else None)
-    # one GPU: ldpc_count_errors adds, so the counters accumulate over the
-    # timed steps (zeroed here, untimed) and are divided by the step count
-    d_ctr.zero_()
-    if launched:
-        dist.barrier()
-    torch.cuda.synchronize()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    dec_ms = []
-    with ClockSampler(dev.index if world == 1 else local) as clk:
-        for i in range(args.steps):
-            if flush is not None:
-                flush.add_(1)                   # evict the previous step's inputs from L2 (untimed)
-            starts[i].record(stream)
-            step()
-            ends[i].record(stream)
-            # decode kernel time of this step (events on the launching stream)
-            ends[i].synchronize()
-            dec_ms.append(ev_d0.elapsed_time(ev_d1))
-        torch.cuda.synchronize()
-    if launched:
-        dist.barrier()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = sum(step_ms)
-    t = torch.tensor([total_ms, sum(dec_ms)], dtype=torch.float64, device=dev)
-    if launched:
-        LD.max_over_ranks(t)
-    total_ms, dec_total_ms = float(t[0]), float(t[1])
-    ctr = d_ctr.cpu().numpy()
-    if not launched:
-        ctr = ctr // max(args.steps, 1)         # identical inputs every step
-    iters_mean = float(ctr[4]) / max(float(ctr[5]), 1.0)
-
-    all_frames = frames * world * args.steps
-    value = all_frames * k / (total_ms / 1e3) / 1e9
-    edge_updates_per_step_rank = float(ctr[4]) / world * wl.edges
-    dec_avg_s = dec_total_ms / args.steps / 1e3
-    achieved = edge_updates_per_step_rank / dec_avg_s / 1e9            # Gedge-updates/s, one GPU
-    clock_mhz = measured_peaks().get("sm_max_mhz", 1965.0)
-    peak = sms * MUFU_PER_CLK_PER_SM * clock_mhz * 1e6 / MUFU_PER_EDGE_UPDATE / 1e9
-    clocks = clk.summary()
-    variant = L.ldpc_decode_variant(code, frames, wl.max_iter, wl.early_term, args.variant)
+    points = list(range(len(wl.ebn0_db))) if args.ebn0 is None else [0]
+    results = [measure_point(args, L, code, wl, p, dev, rank, world, launched, sms, props) for p in points]
+    main_res = results[0]
+    total_ms = sum(r["total_ms"] for r in results)
+    k = main_res["k"]
 
     # ---- end to end through the public API with host buffers (rank-local)
-    e2e = e2e_measure(L, code, wl, args, dev, frame0, k, n, kw, nw, world, frames)
+    e2e = e2e_measure(L, code, wl, args, dev, main_res["frame0"], main_res["count"], k, world)
 
     # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
@@ -507,45 +667,72 @@ def main():
                          f"{dt:.1f} s wall ({dt * threads:.0f} core-s)"}
 
     if rank == 0:
+        ctr = main_res["counters"]
+        frames_all = sum(r["counters"][5] for r in results)
+        launch = "eager" if main_res["graph"] is None else \
+            ("cuda_graph (encode, decode, count)" if main_res["work"].resident
+             else f"cuda_graph ({len(main_res['work'].spans)} chunks x (encode, channel, decode, count))")
         line = {
-            "metric": "decoded info Gbit/s", "value": value, "unit": "Gbit/s", "n_gpus": world,
+            "metric": "decoded info Gbit/s", "value": frames_all * k * args.steps / (total_ms / 1e3) / 1e9,
+            "unit": "Gbit/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded Philox info bits, BPSK/AWGN LLRs; BASELINE.json recipe)",
-            "config": workload_config(wl, frames, world, l2_policy,
-                                      "eager" if graph is None else "cuda_graph (encode, decode, count)"),
-            "edge_updates_per_s": edge_updates_per_step_rank * world / (total_ms / args.steps / 1e3),
-            "decode_ms_per_step": dec_total_ms / args.steps,
-            "mean_iterations": iters_mean, "k": k,
+            "config": workload_config(wl, main_res["count"], world, main_res["l2_policy"], launch, args.scaling,
+                                      main_res["total"], points[0],
+                                      None if main_res["work"].resident else args.chunk),
+            "edge_updates_per_s": sum(r["edge_updates_per_s"] * r["total_ms"] for r in results) / total_ms,
+            "decode_ms_per_step": main_res["dec_ms"] / args.steps,
+            "mean_iterations": ctr[4] / max(ctr[5], 1), "k": k,
             "counters": {"info_bit_errors": int(ctr[0]), "cw_bit_errors": int(ctr[1]),
                          "frame_errors": int(ctr[2]), "undetected": int(ctr[3]), "frames": int(ctr[5])},
-            "roofline": {"bound": "alu", "kernel": f"ldpc_decode variant {variant}: {KERNEL_NAMES.get(variant, '?')}",
-                         "achieved": achieved, "peak": peak,
-                         "unit": "Gedge-updates/s", "frac": achieved / peak, "traffic": dram_traffic(wl, frames),
-                         "peak_basis": f"SFU: {sms} SMs x 16 MUFU/clk x {clock_mhz:.0f} MHz / 4 MUFU per "
-                                       "edge-update (DESIGN.md)"},
+            "roofline": main_res["roofline"],
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "clocks": clocks,
-            # per step: encode_parity + encode_assemble + decode + count
-            "gpu_launches": 4 * args.steps,
+            "clocks": main_res["clocks"],
+            "gpu_launches": (sum(r["launches_per_step"] or 0 for r in results) * args.steps)
+            if main_res["launches_per_step"] is not None else None,
             "setup_s": setup_s,
         }
+        if len(results) > 1:
+            line["points"] = [point_summary(wl, p, r, args.steps) for p, r in zip(points, results)]
+            line["config"]["ebn0_db"] = list(wl.ebn0_db)
+            line["config"]["frame_seed"] = list(wl.frame_seeds)
+            line["config"]["workload"] += f" (sweep {', '.join(str(x) for x in wl.ebn0_db)} dB)"
         print(json.dumps(line), flush=True)
     if launched:
         dist.destroy_process_group()
     return 0
 
 
-def e2e_measure(L, code, wl, args, dev, frame0, k, n, kw, nw, world, frames):
+def point_summary(wl, p, r, steps):
+    c = r["counters"]
+    k = r["k"]
+    return {"ebn0_db": wl.ebn0_db[p], "sigma": wl.sigma(p), "frame_seed": wl.frame_seeds[p],
+            "info_gbit_s": r["value"], "ms_per_step": r["total_ms"] / steps,
+            "decode_ms_per_step": r["dec_ms"] / steps, "mean_iterations": c[4] / max(c[5], 1),
+            "ber_info": c[0] / max(c[5] * k, 1), "fer": c[2] / max(c[5], 1),
+            "undetected": c[3], "frames": c[5],
+            "roofline_frac_on_executed_iterations": r["roofline"]["frac"],
+            "roofline_bound": r["roofline"]["bound"]}
+
+
+def e2e_measure(L, code, wl, args, dev, frame0, count, k, world):
     """Same metric through the public API with pinned host buffers: H2D of the
     step's info bits and LLRs, encode, decode, count, D2H of the decoded bits
-    and the counters, all inside the timed region.  The step is the device
-    arm's batch (`frames`)."""
+    and the counters, all inside the timed region.  Pinned host memory is
+    capped at E2E_PINNED_BYTES over all ranks (the frames beyond it are not
+    part of the e2e sample; C4 fits whole at every N)."""
     import torch
-    F = frames
+    n = code.info.n
+    kw, nw = L.words(k), L.words(n)
+    per_frame = n * 4 + kw * 4 + nw * 4
+    cap = int(E2E_PINNED_BYTES / max(world, 1) / per_frame)
+    F = min(count, cap)
     if args.e2e_frames:
         F = min(F, args.e2e_frames)
+    if F <= 0:
+        return {"value": None, "unit": "Gbit/s", "error": "no frames on this rank"}
     Fc = min(F, args.e2e_chunk)              # pipeline chunk
     nchunks = (F + Fc - 1) // Fc
     try:
@@ -561,7 +748,7 @@ def e2e_measure(L, code, wl, args, dev, frame0, k, n, kw, nw, world, frames):
                  bits=torch.empty((Fc, nw), dtype=torch.int32, device=dev),
                  syn=torch.empty(Fc, dtype=torch.uint8, device=dev),
                  it=torch.empty(Fc, dtype=torch.int32, device=dev)) for _ in range(2)]
-    # the workload's frames, generated once on the device and parked in host memory (untimed)
+    # the rank's frames, generated once on the device and parked in host memory (untimed)
     seed = wl.frame_seeds[0]
     for c in range(nchunks):
         a, m = c * Fc, min(Fc, F - c * Fc)
@@ -608,6 +795,7 @@ def e2e_measure(L, code, wl, args, dev, frame0, k, n, kw, nw, world, frames):
         with torch.cuda.stream(s_out):
             h_ctr.copy_(d_ctr, non_blocking=True)
 
+    s_cmp.wait_stream(torch.cuda.current_stream())
     step()
     torch.cuda.synchronize()
     steps = max(1, args.steps)
@@ -620,12 +808,20 @@ def e2e_measure(L, code, wl, args, dev, frame0, k, n, kw, nw, world, frames):
     end.record(s_in)
     torch.cuda.synchronize()
     ms = start.elapsed_time(end)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    frames_all = torch.tensor([F], dtype=torch.int64, device=dev)
+    from paper_2201_04265_b200 import dist as LD
+    LD.max_over_ranks(t)
+    LD.all_reduce_counters(frames_all)
+    ms = float(t[0])
     bi = F * kw * 4 + F * n * 4
     bo = F * nw * 4 + 6 * 8
-    return {"value": world * steps * F * k / (ms / 1e3) / 1e9, "unit": "Gbit/s", "h2d_bytes_per_step": bi,
+    return {"value": int(frames_all[0]) * steps * k / (ms / 1e3) / 1e9, "unit": "Gbit/s", "h2d_bytes_per_step": bi,
             "d2h_bytes_per_step": bo, "frames_per_gpu_per_step": F,
             "note": f"pinned host buffers; H2D / encode+decode+count / D2H pipelined over {nchunks} chunks of "
-                    f"{Fc} frames on three streams"}
+                    f"{Fc} frames on three streams; max over ranks" +
+                    ("" if F == count else f"; sample of {F} of the rank's {count} frames (pinned-memory cap "
+                                           f"{E2E_PINNED_BYTES / 1e9:.0f} GB over all ranks)")}
 
 
 if __name__ == "__main__":

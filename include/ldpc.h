@@ -250,11 +250,37 @@ ldpc_status ldpc_count_errors(const ldpc_code *code, const uint32_t *d_info,
                               const uint8_t *d_syndrome_ok, const int32_t *d_iters,
                               int64_t frames, int64_t *d_counters6, void *stream);
 
-/* Diagnostics: y[i] = phi(x[i]) with the decoder's own device phi,
- * phi(x) = -ln tanh(x/2) for x >= 0 (the log-domain form of Eq. 5's
- * tanh/atanh pair).  For the exhaustive accuracy sweep in tests.
- * d_x, d_y: count float32 (device). */
+/* Diagnostics: y[i] = phi(x[i]) with the GENERIC CSR decoder's device phi
+ * (spa_decode.cu, variants 1 and 2 only), phi(x) = -ln tanh(x/2) for x >= 0
+ * (the log-domain form of Eq. 5's tanh/atanh pair).  For the
+ * exhaustive accuracy sweep in tests.  d_x, d_y: count float32 (device). */
 ldpc_status ldpc_debug_phi(const float *d_x, float *d_y, int64_t count, void *stream);
+
+/* Diagnostics: the throughput decoders' own phi (every band, exchange-cluster
+ * and lane-per-edge kernel, variants 3-8), which works in log2 units:
+ * psi(y) = log2(e) phi(y ln 2), phi as above (Eq. 5).
+ * d_out[i] = the tier's value at d_y[i] (both count float32, device):
+ *   tier 0 psi        (two regimes, split at y = 1.8033688, selected per element)
+ *   tier 1 psi_small  (C1 - lg2 y + y^2 q(y^2); the regime y <= 1.8033688)
+ *   tier 2 psi_large  (t h(t^2), t = 2^-y;      the regime y >  1.8033688)
+ *   tier 3 psi_deep_large  (h0 2^-y;  voted for warps with every y >= 10)
+ *   tier 4 psi_deep_small  (C1 - lg2 y; voted for warps with every y <= 2^-10)
+ *   tier 5 / 6  the row evaluator with warp votes, first / second psi of a
+ *          check row (the tier is chosen by the votes over each warp's inputs).
+ * LDPC_ERR_ARG for a tier outside 0..6. */
+ldpc_status ldpc_debug_psi(const float *d_y, float *d_out, int64_t count, int32_t tier, void *stream);
+
+/* Diagnostics: the throughput decoders' check-node update (Eq. 5,
+ * P:128-132, readings Q2/Q3/Q7) on `rows` independent rows of `degree`
+ * inputs: d_x[r*degree + j] = L'_vc (log2 units, L' = L log2 e; clamped to
+ * +-30 log2 e inside, as in the decoders); d_e[r*degree + j] = the new
+ * E'_cv = (-1)^degree prod_{j'!=j} sgn(x_j') min(psi(sum_{j'!=j}
+ * psi(|x_j'|)), E_MAX log2 e).  vote != 0 runs the warp-voted tiers
+ * (deep, saturation and clamp) exactly as the fixed-iteration kernels do;
+ * vote == 0 the plain two-regime form (early termination, <= 20 iterations).
+ * degree in {2, 3, 4, 6, 12} (else LDPC_ERR_UNSUPPORTED). */
+ldpc_status ldpc_debug_check_row(const float *d_x, float *d_e, int64_t rows, int32_t degree, int32_t vote,
+                                 void *stream);
 
 /* Work partition, Eq. 9 (corrected per S:336, reading Q6):
  * counts[q] = floor(l/N) + (q < l mod N), displs = exclusive prefix sum.

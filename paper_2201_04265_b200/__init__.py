@@ -20,7 +20,8 @@ __all__ = [
     "Code", "LdpcError", "ldpc_make_H", "ldpc_code_from_csr", "ldpc_make_G", "ldpc_code_query",
     "ldpc_code_copy_H", "ldpc_code_copy_csr", "ldpc_code_copy_perm", "ldpc_code_copy_P",
     "ldpc_code_bind_device", "ldpc_encode", "ldpc_decode_workspace_bytes", "ldpc_decode",
-    "ldpc_gen_info", "ldpc_channel", "ldpc_count_errors", "ldpc_partition", "ldpc_debug_phi", "words",
+    "ldpc_gen_info", "ldpc_channel", "ldpc_count_errors", "ldpc_partition", "ldpc_debug_phi", "ldpc_debug_psi",
+    "ldpc_debug_check_row", "words",
 ]
 
 
@@ -244,6 +245,14 @@ def ldpc_debug_phi(d_x, d_y, count: int, stream=None) -> None:
     call("ldpc_debug_phi", _ptr(d_x), _ptr(d_y), int(count), _stream(stream))
 
 
+def ldpc_debug_psi(d_y, d_out, count: int, tier: int = 0, stream=None) -> None:
+    call("ldpc_debug_psi", _ptr(d_y), _ptr(d_out), int(count), int(tier), _stream(stream))
+
+
+def ldpc_debug_check_row(d_x, d_e, rows: int, degree: int, vote: bool = True, stream=None) -> None:
+    call("ldpc_debug_check_row", _ptr(d_x), _ptr(d_e), int(rows), int(degree), int(bool(vote)), _stream(stream))
+
+
 # ---------------------------------------------------------------- convenience
 @dataclass
 class DecodeOut:
@@ -251,6 +260,7 @@ class DecodeOut:
     syndrome_ok: "object"
     iters: "object"
     posterior: "object"
+    workspace: "object" = None     # kept alive with the outputs (the launch may still be running)
 
 
 def decode(code: Code, llr, max_iter: int = 50, early_term: bool = False, posterior: bool = False,
@@ -267,4 +277,6 @@ def decode(code: Code, llr, max_iter: int = 50, early_term: bool = False, poster
     wsb = ldpc_decode_workspace_bytes(code, frames, max_iter, early_term, variant)
     ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev) if wsb else None
     ldpc_decode(code, llr, frames, bits, syn, its, post, ws, max_iter, early_term, variant, stream)
-    return DecodeOut(bits, syn, its, post)
+    if ws is not None and stream is not None:
+        ws.record_stream(stream)     # the caching allocator must not reuse it before `stream` finishes
+    return DecodeOut(bits, syn, its, post, ws)

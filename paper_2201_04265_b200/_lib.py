@@ -20,7 +20,7 @@ EXPORTED = [
     "ldpc_code_copy_csr", "ldpc_code_copy_perm", "ldpc_code_copy_P", "ldpc_code_bind_device",
     "ldpc_code_free", "ldpc_status_str", "ldpc_encode", "ldpc_decode_workspace_bytes", "ldpc_decode",
     "ldpc_decode_variant", "ldpc_decode_simulate",
-    "ldpc_gen_info", "ldpc_channel", "ldpc_count_errors", "ldpc_partition", "ldpc_debug_phi",
+    "ldpc_gen_info", "ldpc_channel", "ldpc_count_errors", "ldpc_partition", "ldpc_debug_phi", "ldpc_debug_psi", "ldpc_debug_check_row",
 ]
 
 
@@ -76,6 +76,8 @@ def lib() -> C.CDLL:
             "ldpc_count_errors": [vp, vp, vp, vp, vp, vp, i64, vp, vp],
             "ldpc_partition": [i64, i32, vp, vp],
             "ldpc_debug_phi": [vp, vp, i64, vp],
+            "ldpc_debug_psi": [vp, vp, i64, i32, vp],
+            "ldpc_debug_check_row": [vp, vp, i64, i32, i32, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)

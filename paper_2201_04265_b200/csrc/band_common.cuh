@@ -56,6 +56,12 @@ __device__ __forceinline__ float psi_large(float y) {
     const float u = t * t;
     return t * fmaf(fmaf(fmaf(kH3, u, kH2), u, kH1), u, kH0);
 }
+// Deep-converged tiers (psi_row's votes take them only when the whole warp's
+// inputs lie in their domain): y >= kUltraLargeB -> h0 2^-y (dropped terms
+// <= 3.2e-7 relative); y <= kUltraSmallB -> C1 - lg2 y (dropped term
+// <= 5.5e-8 against psi >= 11.5).  One SFU op and one FMA-pipe op each.
+__device__ __forceinline__ float psi_deep_large(float y) { return kH0 * ex2a(-y); }
+__device__ __forceinline__ float psi_deep_small(float y) { return kC1 - lg2a(y); }
 
 // psi over a row.  When every input of every active lane of the warp falls in
 // one regime -- the common case once a frame has converged: |L_vc| large
@@ -78,12 +84,10 @@ __device__ __forceinline__ void psi_row(const float (&in)[D], float (&out)[D]) {
         if (LARGE_FIRST) lo = fminf(lo, in[j]);
         else hi = fmaxf(hi, in[j]);
     }
-    // Deep-converged tiers: y >= 10 -> psi = h0 2^-y (dropped terms <= 3.2e-7
-    // relative); y <= 2^-10 -> psi = C1 - lg2 y (dropped term <= 5.5e-8 against
-    // psi >= 11.5).  One SFU op and one FMA-pipe op per input.
+    // deep-converged tiers (psi_deep_large / psi_deep_small)
     if (LARGE_FIRST ? __all_sync(act, lo >= kUltraLargeB) : __all_sync(act, hi <= kUltraSmallB)) {
 #pragma unroll
-        for (int j = 0; j < D; ++j) out[j] = LARGE_FIRST ? kH0 * ex2a(-in[j]) : kC1 - lg2a(in[j]);
+        for (int j = 0; j < D; ++j) out[j] = LARGE_FIRST ? psi_deep_large(in[j]) : psi_deep_small(in[j]);
         return;
     }
     if (LARGE_FIRST ? __all_sync(act, lo > kSplitB) : __all_sync(act, hi <= kSplitB)) {

@@ -60,7 +60,8 @@ def test_make_H_bit_exact(L, oracle, n, wc, wr, seed):
     assert info.max_row_deg == wr and info.max_col_deg == wc
 
 
-@pytest.mark.parametrize("n,wc,wr", [(96, 3, 6), (1008, 3, 6), (3996, 3, 4), (3996, 3, 12), (1032, 9, 12)])
+@pytest.mark.parametrize("n,wc,wr", [(96, 3, 6), (1008, 3, 6), (3996, 3, 4), (3996, 3, 6), (3996, 3, 12),
+                                     (1032, 9, 12), (1032, 6, 12), (1032, 3, 12), (16200, 3, 6)])
 def test_make_G_bit_exact(L, oracle, n, wc, wr):
     lib_code = L.ldpc_make_G(L.ldpc_make_H(n, wc, wr, 1))
     ora = oracle.make_H(n, wc, wr, 1).make_G()

@@ -195,6 +195,39 @@ def test_encode_codewords_linear(oracle, n, wc, wr):
         assert oracle.syndrome_zero(code, ca[f])
 
 
+def test_syndrome_zero_pinned(oracle):
+    """Eq. 1: syndrome_zero(z) is 1 exactly when H z^T = 0 over
+    GF(2).  Against numpy's integer product and brute-force enumeration: every
+    weight-1 word is rejected (no H here has an all-zero column), every
+    codeword of Fig. 1 and Hamming(7,4) is accepted, and random
+    words of a Gallager code agree with (H z) mod 2 -- so an always-true (or
+    always-false) syndrome fails."""
+    mats = [hp.golden_matrix("fig1_H.txt"), hp.hamming74_H()]
+    for H in mats:
+        code = oracle.Code.from_dense(H)
+        n = H.shape[1]
+        for v in range(n):
+            e = np.zeros(n, np.uint8)
+            e[v] = 1
+            assert not oracle.syndrome_zero(code, e)
+        cws = hp.codewords(H)
+        assert len(cws) > 1
+        for c in cws:
+            assert oracle.syndrome_zero(code, c)
+        words = ((np.arange(1 << n)[:, None] >> np.arange(n)[None, :]) & 1).astype(np.uint8)
+        want = np.all((words.astype(np.int64) @ H.T.astype(np.int64)) % 2 == 0, axis=1)
+        got = np.array([oracle.syndrome_zero(code, w) for w in words])
+        assert np.array_equal(got, want)
+        assert 0 < want.sum() < len(words)
+    code = oracle.make_H(96, 3, 6, 1)
+    H = code.dense().astype(np.int64)
+    rng = np.random.default_rng(5)
+    z = rng.integers(0, 2, (200, 96), dtype=np.uint8)
+    for f in range(200):
+        assert oracle.syndrome_zero(code, z[f]) == (not np.any((H @ z[f].astype(np.int64)) % 2))
+    assert not any(oracle.syndrome_zero(code, z[f]) for f in range(200))     # random words fail
+
+
 # ----------------------------------------------------------------- channel
 def test_llr_spec_examples(oracle):
     """Eq. 4: R = 2y/sigma^2; SPEC S:289-291 examples."""
@@ -424,6 +457,7 @@ def test_spa_early_termination_consistent_with_fixed_trace(oracle):
     decision has zero syndrome in the fixed-iteration trace, and the outputs
     equal the fixed-mode outputs at that t."""
     code = oracle.make_H(96, 3, 6, 1).make_G()
+    H = code.dense().astype(np.int64)
     info = oracle.gen_info(21, 0, 6, code.k)
     R = oracle.channel(22, 0, oracle.encode(code, info), 0.85)
     Le, ze, ite, soe = oracle.spa_decode(code, R, 30, early_term=True)
@@ -431,7 +465,7 @@ def test_spa_early_termination_consistent_with_fixed_trace(oracle):
         first = None
         for t in range(1, 31):
             L, z, it, so = oracle.spa_decode(code, R[f], t)
-            if oracle.syndrome_zero(code, z[0]):
+            if not np.any((H @ z[0].astype(np.int64)) % 2):      # Eq. 1 by numpy, not the oracle
                 first = t
                 assert np.array_equal(L[0], Le[f]) and np.array_equal(z[0], ze[f])
                 break
