@@ -69,6 +69,7 @@ def parse():
                     help="override the config's early termination (measurement variant)")
     ap.add_argument("--ebn0", type=float, default=None, help="override the config's Eb/N0 in dB (measurement variant)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end arm (profiling runs)")
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--eager", action="store_true", help="launch the step's kernels eagerly instead of replaying a CUDA graph")
     ap.add_argument("--mode", choices=["batch", "stream", "simulate"], default="batch",
@@ -474,6 +475,8 @@ class RankWork:
         self.d_ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev) if wsb else None
         self.ev = [(torch.cuda.Event(enable_timing=True, external=True),
                     torch.cuda.Event(enable_timing=True, external=True)) for _ in self.spans]
+        self.eve = [(torch.cuda.Event(enable_timing=True, external=True),
+                     torch.cuda.Event(enable_timing=True, external=True)) for _ in self.spans]
         if count:
             L.ldpc_gen_info(self.seed, frame0, count, self.k, self.d_info)
             if self.resident:
@@ -485,12 +488,14 @@ class RankWork:
         L, code, wl = self.L, self.code, self.wl
         with torch.cuda.stream(s):
             self.d_ctr.zero_()
-        for (f0, m), (e0, e1) in zip(self.spans, self.ev):
+        for (f0, m), (e0, e1), (g0, g1) in zip(self.spans, self.ev, self.eve):
             if m == 0:
                 continue
             a = f0 - self.frame0
             info = self.d_info[a:a + m]
+            g0.record(s)
             L.ldpc_encode(code, info, self.d_cw, m, stream=s)
+            g1.record(s)
             if not self.resident:
                 L.ldpc_channel(code, self.seed, f0, m, self.d_cw, self.sigma, self.d_llr, stream=s)
             e0.record(s)
@@ -502,27 +507,33 @@ class RankWork:
     def decode_ms(self):
         return sum(e0.elapsed_time(e1) for (f0, m), (e0, e1) in zip(self.spans, self.ev) if m)
 
+    def encode_ms(self):
+        return sum(e0.elapsed_time(e1) for (f0, m), (e0, e1) in zip(self.spans, self.eve) if m)
+
 
 def graph_kernel_launches(graph):
-    """Kernel nodes of a captured step that are this library's (not torch's
-    fill kernels): counted from the CUDA graph itself."""
+    """Kernel nodes of a captured step that are this library's (torch's own
+    fill kernels excluded): counted from the CUDA graph itself, by name
+    (driver API: cuGraphGetNodes / cuGraphKernelNodeGetParams / cuFuncGetName)."""
     try:
-        from cuda.bindings import runtime as rt
+        from cuda.bindings import driver as drv
         g = graph.raw_cuda_graph()
-        err, nodes, num = rt.cudaGraphGetNodes(g, 0)
-        err, nodes, num = rt.cudaGraphGetNodes(g, num)
+        g = drv.CUgraph(init_value=int(g)) if not isinstance(g, drv.CUgraph) else g
+        err, nodes, num = drv.cuGraphGetNodes(g, 0)
+        err, nodes, num = drv.cuGraphGetNodes(g, num)
         ours = 0
         for nd in nodes:
-            err, ty = rt.cudaGraphNodeGetType(nd)
-            if ty != rt.cudaGraphNodeType.cudaGraphNodeTypeKernel:
+            err, ty = drv.cuGraphNodeGetType(nd)
+            if ty != drv.CUgraphNodeType.CU_GRAPH_NODE_TYPE_KERNEL:
                 continue
-            err, prm = rt.cudaGraphKernelNodeGetParams(nd)
-            err, name = rt.cudaFuncGetName(prm.func)
+            err, prm = drv.cuGraphKernelNodeGetParams(nd)
+            err, name = drv.cuFuncGetName(prm.func)
             name = name.decode() if isinstance(name, bytes) else str(name)
             if "ldpc" in name:
                 ours += 1
         return ours
-    except Exception:
+    except Exception as e:     # pragma: no cover
+        print(f"bench: could not count the graph's kernel nodes: {e!r}", file=sys.stderr)
         return None
 
 
@@ -545,7 +556,7 @@ def measure_point(args, L, code, wl, point, dev, rank, world, launched, sms, pro
     torch.cuda.synchronize()
     graph, launches = None, None
     if not args.eager:
-        graph = torch.cuda.CUDAGraph()
+        graph = torch.cuda.CUDAGraph(keep_graph=True)
         cap = torch.cuda.Stream()
         cap.wait_stream(stream)
         with torch.cuda.stream(cap):
@@ -553,6 +564,7 @@ def measure_point(args, L, code, wl, point, dev, rank, world, launched, sms, pro
                 work.device_work(cap)
         torch.cuda.synchronize()
         launches = graph_kernel_launches(graph)
+        graph.instantiate()
 
     def step():
         if graph is not None:
@@ -579,7 +591,7 @@ def measure_point(args, L, code, wl, point, dev, rank, world, launched, sms, pro
     torch.cuda.synchronize()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    dec_ms = []
+    dec_ms, enc_ms = [], []
     with ClockSampler(dev.index) as clk:
         for i in range(args.steps):
             if flush is not None:
@@ -589,14 +601,15 @@ def measure_point(args, L, code, wl, point, dev, rank, world, launched, sms, pro
             ends[i].record(stream)
             ends[i].synchronize()
             dec_ms.append(work.decode_ms())     # decode kernel time of this step
+            enc_ms.append(work.encode_ms())     # encode kernels (parity + assemble)
             ctr_total.add_(work.d_ctr)
         torch.cuda.synchronize()
     if launched:
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    t = torch.tensor([sum(step_ms), sum(dec_ms)], dtype=torch.float64, device=dev)
+    t = torch.tensor([sum(step_ms), sum(dec_ms), sum(enc_ms)], dtype=torch.float64, device=dev)
     reduce_step(None, t)                        # max over ranks (counters were summed every step)
-    total_ms, dec_total_ms = float(t[0]), float(t[1])
+    total_ms, dec_total_ms, enc_total_ms = float(t[0]), float(t[1]), float(t[2])
     ctr = (ctr_total.cpu().numpy() // max(args.steps, 1)).tolist()   # per step, all ranks
     k = work.k
     variant = L.ldpc_decode_variant(code, work.Fb, wl.max_iter, wl.early_term, args.variant)
@@ -611,8 +624,34 @@ def measure_point(args, L, code, wl, point, dev, rank, world, launched, sms, pro
         "edge_updates_per_s": ctr[4] * wl.edges * args.steps / (total_ms / 1e3),
         "roofline": roofline(wl, variant, achieved, sms, clock_mhz, work.Fb), "clocks": clk.summary(),
         "l2_policy": l2_policy, "total": total,
+        "encode": encode_roofline(work, count, enc_total_ms / args.steps, sms, clock_mhz),
     }
     return res
+
+
+def encode_roofline(work, count, enc_ms, sms, clock_mhz):
+    """Encode (e1, Eq. 3): the parity bits are M.P over GF(2), one
+    LOP3 (acc ^= m & p) per 32 bit-MACs: (n - k) ceil(k/32) LOP3 per frame,
+    on the INT/ALU pipe; peak = the LOP3 rate measured by
+    tools/microbench_lop.cu (profiles/peaks_extra.json)."""
+    if enc_ms <= 0 or count == 0:
+        return None
+    kw = (work.k + 31) // 32
+    ops = float(count) * (work.n - work.k) * kw
+    per_clk, basis = 64.0, "assumed 64 LOP3/clk/SM (ALU pipe, 16 lanes/clk/SMSP)"
+    try:
+        with open(os.path.join(ROOT, "profiles", "peaks_extra.json")) as f:
+            px = json.load(f)
+        per_clk = float(px["lop3_per_clk_per_sm"])
+        basis = f"measured {per_clk:.1f} LOP3/clk/SM (tools/microbench_lop.cu, profiles/peaks_extra.json)"
+    except Exception:
+        pass
+    peak = sms * per_clk * clock_mhz * 1e6 / 1e12
+    ach = ops / (enc_ms / 1e3) / 1e12
+    return {"bound": "alu", "kernel": "encode_parity_kernel + encode_assemble_kernel (ldpc_encode)",
+            "achieved": ach, "peak": peak, "unit": "T LOP3/s", "frac": ach / peak, "ms_per_step": enc_ms,
+            "algorithmic_ops_per_frame": (work.n - work.k) * kw,
+            "peak_basis": f"{sms} SMs x {basis} x {clock_mhz:.0f} MHz"}
 
 
 def main():
@@ -654,7 +693,8 @@ def main():
     k = main_res["k"]
 
     # ---- end to end through the public API with host buffers (rank-local)
-    e2e = e2e_measure(L, code, wl, args, dev, main_res["frame0"], main_res["count"], k, world)
+    e2e = None if args.no_e2e else e2e_measure(L, code, wl, args, dev, main_res["frame0"], main_res["count"], k,
+                                               world)
 
     # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
@@ -687,6 +727,7 @@ def main():
             "counters": {"info_bit_errors": int(ctr[0]), "cw_bit_errors": int(ctr[1]),
                          "frame_errors": int(ctr[2]), "undetected": int(ctr[3]), "frames": int(ctr[5])},
             "roofline": main_res["roofline"],
+            "encode_roofline": main_res["encode"],
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": main_res["clocks"],
