@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libldpc_b200.so")
+LIB_PATH = os.environ.get("LDPC_LIB_PATH") or os.path.join(_HERE, "libldpc_b200.so")   # override: A/B of builds
 
 # symbols declared in include/ldpc.h (a CPU test checks the two lists agree)
 EXPORTED = [

@@ -8,6 +8,10 @@
 
 #include <cstdint>
 
+#ifndef LDPC_SCALAR_PSI
+#define LDPC_SCALAR_PSI 0      // 1: psi pairs evaluated with scalar fp32 ops (A/B builds; results identical)
+#endif
+
 namespace ldpc {
 namespace band {
 
@@ -63,6 +67,99 @@ __device__ __forceinline__ float psi_large(float y) {
 __device__ __forceinline__ float psi_deep_large(float y) { return kH0 * ex2a(-y); }
 __device__ __forceinline__ float psi_deep_small(float y) { return kC1 - lg2a(y); }
 
+// ---------------------------------------------------------------------------
+// Packed evaluation (sm_100a FFMA2 / FMUL2 / FADD2: two fp32 lanes per
+// instruction).  The decoders are issue-bound (profiles/issue.json), and psi's
+// polynomial arithmetic is most of a non-converged row's instructions; a row's
+// elements are evaluated in pairs with the .f32x2 forms of exactly the scalar
+// operations above (same operands, same order, .rn each), so every element's
+// result is bit-identical to psi / psi_small / psi_large / psi_deep_* -- only
+// the issue count halves.  The MUFU ops and the regime select stay scalar.
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2_pack(float lo, float hi) {
+    f2_t r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void f2_unpack(f2_t v, float &lo, float &hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2_t f2_splat(float c) { return f2_pack(c, c); }
+__device__ __forceinline__ f2_t f2_fma(f2_t a, f2_t b, f2_t c) {
+    f2_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f2_t f2_mul(f2_t a, f2_t b) {
+    f2_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2_t f2_add(f2_t a, f2_t b) {
+    f2_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2_t f2_sub(f2_t a, f2_t b) {
+    f2_t d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+
+enum PsiTier { kPsiFull = 0, kPsiSmall, kPsiLarge, kPsiDeepLarge, kPsiDeepSmall };
+
+// small regime of a pair: fmaf(s, q(s), C1) - lg2(y), s = y^2
+__device__ __forceinline__ f2_t psi2_small(f2_t y, float y0, float y1) {
+    const f2_t s = f2_mul(y, y);
+    const f2_t q = f2_fma(f2_fma(f2_fma(f2_splat(kQ3), s, f2_splat(kQ2)), s, f2_splat(kQ1)), s, f2_splat(kQ0));
+    return f2_sub(f2_fma(s, q, f2_splat(kC1)), f2_pack(lg2a(y0), lg2a(y1)));
+}
+// large regime of a pair: t h(t^2), t = 2^-y
+__device__ __forceinline__ f2_t psi2_large(float y0, float y1) {
+    const f2_t t = f2_pack(ex2a(-y0), ex2a(-y1));
+    const f2_t u = f2_mul(t, t);
+    return f2_mul(t, f2_fma(f2_fma(f2_fma(f2_splat(kH3), u, f2_splat(kH2)), u, f2_splat(kH1)), u, f2_splat(kH0)));
+}
+template <int TIER>
+__device__ __forceinline__ float psi1(float y) {
+    if constexpr (TIER == kPsiFull) return psi(y);
+    else if constexpr (TIER == kPsiSmall) return psi_small(y);
+    else if constexpr (TIER == kPsiLarge) return psi_large(y);
+    else if constexpr (TIER == kPsiDeepLarge) return psi_deep_large(y);
+    else return psi_deep_small(y);
+}
+template <int TIER>
+__device__ __forceinline__ void psi2(float y0, float y1, float &o0, float &o1) {
+    const f2_t y = f2_pack(y0, y1);
+    if constexpr (TIER == kPsiFull) {
+        float s0, s1, l0, l1;
+        f2_unpack(psi2_small(y, y0, y1), s0, s1);
+        f2_unpack(psi2_large(y0, y1), l0, l1);
+        o0 = y0 > kSplitB ? l0 : s0;
+        o1 = y1 > kSplitB ? l1 : s1;
+    } else if constexpr (TIER == kPsiSmall) {
+        f2_unpack(psi2_small(y, y0, y1), o0, o1);
+    } else if constexpr (TIER == kPsiLarge) {
+        f2_unpack(psi2_large(y0, y1), o0, o1);
+    } else if constexpr (TIER == kPsiDeepLarge) {
+        f2_unpack(f2_mul(f2_splat(kH0), f2_pack(ex2a(-y0), ex2a(-y1))), o0, o1);
+    } else {
+        f2_unpack(f2_sub(f2_splat(kC1), f2_pack(lg2a(y0), lg2a(y1))), o0, o1);
+    }
+}
+// one tier over a row: pairs packed, an odd last element scalar
+template <int D, int TIER>
+__device__ __forceinline__ void psi_eval(const float (&in)[D], float (&out)[D]) {
+#if LDPC_SCALAR_PSI
+#pragma unroll
+    for (int j = 0; j < D; ++j) out[j] = psi1<TIER>(in[j]);
+#else
+#pragma unroll
+    for (int j = 0; j + 1 < D; j += 2) psi2<TIER>(in[j], in[j + 1], out[j], out[j + 1]);
+    if constexpr (D & 1) out[D - 1] = psi1<TIER>(in[D - 1]);
+#endif
+}
+
 // psi over a row.  When every input of every active lane of the warp falls in
 // one regime -- the common case once a frame has converged: |L_vc| large
 // (first psi), exclusive sums tiny (second psi) -- only that regime is
@@ -73,8 +170,7 @@ __device__ __forceinline__ float psi_deep_small(float y) { return kC1 - lg2a(y);
 template <int D, bool LARGE_FIRST, bool VOTE>
 __device__ __forceinline__ void psi_row(const float (&in)[D], float (&out)[D]) {
     if (!VOTE) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) out[j] = psi(in[j]);
+        psi_eval<D, kPsiFull>(in, out);
         return;
     }
     const unsigned act = __activemask();
@@ -86,13 +182,11 @@ __device__ __forceinline__ void psi_row(const float (&in)[D], float (&out)[D]) {
     }
     // deep-converged tiers (psi_deep_large / psi_deep_small)
     if (LARGE_FIRST ? __all_sync(act, lo >= kUltraLargeB) : __all_sync(act, hi <= kUltraSmallB)) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) out[j] = LARGE_FIRST ? psi_deep_large(in[j]) : psi_deep_small(in[j]);
+        psi_eval<D, LARGE_FIRST ? kPsiDeepLarge : kPsiDeepSmall>(in, out);
         return;
     }
     if (LARGE_FIRST ? __all_sync(act, lo > kSplitB) : __all_sync(act, hi <= kSplitB)) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) out[j] = LARGE_FIRST ? psi_large(in[j]) : psi_small(in[j]);
+        psi_eval<D, LARGE_FIRST ? kPsiLarge : kPsiSmall>(in, out);
         return;
     }
 #pragma unroll
@@ -101,12 +195,10 @@ __device__ __forceinline__ void psi_row(const float (&in)[D], float (&out)[D]) {
         else lo = fminf(lo, in[j]);
     }
     if (LARGE_FIRST ? __all_sync(act, hi <= kSplitB) : __all_sync(act, lo > kSplitB)) {
-#pragma unroll
-        for (int j = 0; j < D; ++j) out[j] = LARGE_FIRST ? psi_small(in[j]) : psi_large(in[j]);
+        psi_eval<D, LARGE_FIRST ? kPsiSmall : kPsiLarge>(in, out);
         return;
     }
-#pragma unroll
-    for (int j = 0; j < D; ++j) out[j] = psi(in[j]);
+    psi_eval<D, kPsiFull>(in, out);
 }
 
 // Exclusive sums Phi_j = sum_{k != j} f_k of positive terms: never
