@@ -168,10 +168,10 @@ __device__ __forceinline__ void psi_eval(const float (&in)[D], float (&out)[D]) 
 // under early termination: a frame stops as soon as it converges, so the
 // uniform regime never lasts and the votes would be pure overhead.
 template <int D, bool LARGE_FIRST, bool VOTE>
-__device__ __forceinline__ void psi_row(const float (&in)[D], float (&out)[D]) {
+__device__ __forceinline__ bool psi_row(const float (&in)[D], float (&out)[D]) {
     if (!VOTE) {
         psi_eval<D, kPsiFull>(in, out);
-        return;
+        return false;
     }
     const unsigned act = __activemask();
     float lo = in[0], hi = in[0];
@@ -183,11 +183,11 @@ __device__ __forceinline__ void psi_row(const float (&in)[D], float (&out)[D]) {
     // deep-converged tiers (psi_deep_large / psi_deep_small)
     if (LARGE_FIRST ? __all_sync(act, lo >= kUltraLargeB) : __all_sync(act, hi <= kUltraSmallB)) {
         psi_eval<D, LARGE_FIRST ? kPsiDeepLarge : kPsiDeepSmall>(in, out);
-        return;
+        return true;
     }
     if (LARGE_FIRST ? __all_sync(act, lo > kSplitB) : __all_sync(act, hi <= kSplitB)) {
         psi_eval<D, LARGE_FIRST ? kPsiLarge : kPsiSmall>(in, out);
-        return;
+        return true;
     }
 #pragma unroll
     for (int j = 1; j < D; ++j) {
@@ -196,9 +196,10 @@ __device__ __forceinline__ void psi_row(const float (&in)[D], float (&out)[D]) {
     }
     if (LARGE_FIRST ? __all_sync(act, hi <= kSplitB) : __all_sync(act, lo > kSplitB)) {
         psi_eval<D, LARGE_FIRST ? kPsiSmall : kPsiLarge>(in, out);
-        return;
+        return true;
     }
     psi_eval<D, kPsiFull>(in, out);
+    return false;
 }
 
 // Exclusive sums Phi_j = sum_{k != j} f_k of positive terms: never
@@ -207,6 +208,25 @@ __device__ __forceinline__ void psi_row(const float (&in)[D], float (&out)[D]) {
 // suffix otherwise (a tree for D = 12 measured -0.6 on C3-R3/4).
 template <int D>
 __device__ __forceinline__ void exclusive_sums(const float (&f)[D], float (&ex)[D]) {
+#if !LDPC_SCALAR_PSI
+    // the same sums, pairs of outputs on the packed pipe (each element's
+    // operands and order unchanged: bit-identical)
+    if constexpr (D == 6) {
+        const float a01 = f[0] + f[1], a23 = f[2] + f[3], a45 = f[4] + f[5];
+        float o01, o23;
+        f2_unpack(f2_add(f2_pack(a23, a01), f2_splat(a45)), o01, o23);
+        const float o45 = a01 + a23;
+        f2_unpack(f2_add(f2_pack(f[1], f[0]), f2_splat(o01)), ex[0], ex[1]);
+        f2_unpack(f2_add(f2_pack(f[3], f[2]), f2_splat(o23)), ex[2], ex[3]);
+        f2_unpack(f2_add(f2_pack(f[5], f[4]), f2_splat(o45)), ex[4], ex[5]);
+        return;
+    } else if constexpr (D == 4) {
+        const float a01 = f[0] + f[1], a23 = f[2] + f[3];
+        f2_unpack(f2_add(f2_pack(f[1], f[0]), f2_splat(a23)), ex[0], ex[1]);
+        f2_unpack(f2_add(f2_pack(f[3], f[2]), f2_splat(a01)), ex[2], ex[3]);
+        return;
+    }
+#endif
     if constexpr (D == 6) {
         const float a01 = f[0] + f[1], a23 = f[2] + f[3], a45 = f[4] + f[5];
         const float o01 = a23 + a45, o23 = a01 + a45, o45 = a01 + a23;
@@ -276,7 +296,7 @@ __host__ __device__ constexpr bool has_clamp_tier() { return sat_bound<D>() > kC
 // cm: the row's clamp magnitudes (clamp_row_mags, shared memory; used when
 // has_clamp_tier<D>() and VOTE; may be null otherwise).
 template <int D, bool VOTE>
-__device__ __forceinline__ void check_row(const float (&x)[D], float (&e)[D], const float *cm = nullptr) {
+__device__ __forceinline__ bool check_row(const float (&x)[D], float (&e)[D], const float *cm = nullptr) {
     float f[D], ax[D];
     uint32_t sx = (D & 1) ? 0x80000000u : 0u;     // (-1)^{d_c}
 #pragma unroll
@@ -294,7 +314,7 @@ __device__ __forceinline__ void check_row(const float (&x)[D], float (&e)[D], co
 #pragma unroll
             for (int j = 0; j < D; ++j)
                 e[j] = __uint_as_float(__float_as_uint(kEMaxB) | ((sx ^ __float_as_uint(x[j])) & 0x80000000u));
-            return;
+            return true;
         }
     }
     if constexpr (VOTE && has_clamp_tier<D>()) {
@@ -305,20 +325,34 @@ __device__ __forceinline__ void check_row(const float (&x)[D], float (&e)[D], co
 #pragma unroll
             for (int j = 0; j < D; ++j)
                 e[j] = __uint_as_float(__float_as_uint(cm[j]) | ((sx ^ __float_as_uint(x[j])) & 0x80000000u));
-            return;
+            return true;
         }
     }
-    psi_row<D, true, VOTE>(ax, f);
+    bool hit = psi_row<D, true, VOTE>(ax, f);
     float ex[D];
     exclusive_sums<D>(f, ex);
     float g[D];
-    psi_row<D, false, VOTE>(ex, g);
+    hit |= psi_row<D, false, VOTE>(ex, g);
 #pragma unroll
     for (int j = 0; j < D; ++j) {
         const float mag = fminf(g[j], kEMaxB);
         const uint32_t sgn = (sx ^ __float_as_uint(x[j])) & 0x80000000u;
         e[j] = __uint_as_float(__float_as_uint(mag) | sgn);
     }
+    return hit;
+}
+
+// Adaptive votes (kernels whose frames stay unconverged for long stretches,
+// e.g. C5 at 1.2 dB): vote_now (warp-uniform) selects the voted update
+// (tiers; returns whether one was taken) or the plain two-regime one, whose
+// vote instructions would be pure overhead on rows that straddle regimes.
+// Both are Eq. 5 within the psi error budget (tests/test_gpu_psi.py).
+template <int D>
+__device__ __forceinline__ bool check_row_gated(const float (&x)[D], float (&e)[D], bool vote_now,
+                                                const float *cm = nullptr) {
+    if (vote_now) return check_row<D, true>(x, e, cm);
+    check_row<D, false>(x, e);
+    return false;
 }
 
 // check_row split over a lane pair (band_kernel LPR = 2): lane h = lane & 1

@@ -131,6 +131,7 @@ struct XArgs {
     const float *llr;
     int64_t frames;
     int32_t max_iter;
+    int32_t adapt_votes;    // xband2: psi votes only after a hit (or every 4th iteration)
     uint32_t *bits;
     uint8_t *syn_ok;
     int32_t *iters;
@@ -542,6 +543,9 @@ __global__ void __launch_bounds__(MAXT, 1) xband2_kernel(const XArgs a) {
         const int ns = fs[1] < a.frames ? 2 : 1;    // cluster-uniform
         float e0[2][WR];
         uint32_t synd[2] = {0, 0};
+        // adaptive psi votes (warp-uniform): vote in iteration t only if a
+        // vote hit in iteration t - 1 or t = 1 mod 4
+        bool vote_on[2] = {true, true}, hit[2] = {false, false};
         if (producer) {
             for (int sl = 0; sl < ns; ++sl) ship_l(sl);
             for (int t = 1; t <= a.max_iter; ++t) {
@@ -576,6 +580,10 @@ __global__ void __launch_bounds__(MAXT, 1) xband2_kernel(const XArgs a) {
 #pragma unroll
                 for (int sl = 0; sl < 2; ++sl) {
                     if (sl < ns) {
+                        if (a.adapt_votes) {
+                            vote_on[sl] = hit[sl] || (t & 3) == 1;
+                            hit[sl] = false;
+                        }
                         wait_row(sl);
 #pragma unroll
                         for (int b = 0; b < NB; ++b) {
@@ -587,7 +595,7 @@ __global__ void __launch_bounds__(MAXT, 1) xband2_kernel(const XArgs a) {
                                 float x[WR], e[WR];
 #pragma unroll
                                 for (int j = 0; j < WR; ++j) x[j] = *reinterpret_cast<const float *>(rowr[sl] + s_[j]);
-                                check_row<WR, true>(x, e);
+                                hit[sl] |= check_row_gated<WR>(x, e, vote_on[sl]);
 #pragma unroll
                                 for (int j = 0; j < WR; ++j) *reinterpret_cast<float *>(rowr[sl] + s_[j]) = e[j];
                             }
@@ -640,7 +648,7 @@ __global__ void __launch_bounds__(MAXT, 1) xband2_kernel(const XArgs a) {
                             }
                         }
                         chunk_done(vchunk(sl));
-                        if (own && !last) check_row<WR, true>(lv, e0[sl]);
+                        if (own && !last) hit[sl] |= check_row_gated<WR>(lv, e0[sl], vote_on[sl]);
                     }
                 }
             }
@@ -802,6 +810,7 @@ ldpc_status xcluster_launch(const ldpc_code &c, const XClusterPlan &p, const flo
     a.llr = llr;
     a.frames = frames;
     a.max_iter = o.max_iter;
+    a.adapt_votes = std::getenv("LDPC_XVOTE_ALWAYS") ? 0 : 1;
     a.bits = bits;
     a.syn_ok = syn;
     a.iters = iters;

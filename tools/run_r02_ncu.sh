@@ -1,8 +1,18 @@
-# r02: full ncu captures of the decode launch for C2 (1.0 dB, 10k frames), C3-R1/2, C5 (one chunk), C4; FFMA2 microbench
+# r02: full ncu captures of the decode launch; summaries, raw metrics and (C5) the SASS source page
+# are written to gpurun_out/ and the .ncu-rep files removed (gpurun brings back <= 64 MiB)
 mkdir -p gpurun_out
 ./tools/microbench_ffma2 > gpurun_out/p_ffma2.txt 2>&1
 K="regex:band_kernel|xband"
-timeout 900 ncu --set full --clock-control none --import-source on -k "$K" -c 1 -o gpurun_out/ncu_c2 -f python bench.py --config C2 --ebn0 1.0 --steps 1 --warmup 0 --eager --no-cpu-baseline --no-e2e > gpurun_out/ncu_c2.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k "$K" -c 1 -o gpurun_out/ncu_c5 -f python bench.py --config C5 --frames 16384 --steps 1 --warmup 0 --eager --no-cpu-baseline --no-e2e > gpurun_out/ncu_c5.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k "$K" -c 1 -o gpurun_out/ncu_c3r12 -f python bench.py --config C3-R1/2 --steps 1 --warmup 0 --eager --no-cpu-baseline --no-e2e > gpurun_out/ncu_c3r12.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k "$K" -c 1 -o gpurun_out/ncu_c4 -f python bench.py --frames 32768 --steps 1 --warmup 0 --eager --no-cpu-baseline --no-e2e > gpurun_out/ncu_c4.log 2>&1
+cap() {  # tag, bench args...
+  tag=$1; shift
+  timeout 900 ncu --set full --clock-control none --import-source on -k "$K" -c 1 -o /tmp/ncu_$tag -f python bench.py "$@" --steps 1 --warmup 0 --eager --no-cpu-baseline --no-e2e > gpurun_out/ncu_$tag.log 2>&1
+  python tools/ncu_summary.py full /tmp/ncu_$tag.ncu-rep > gpurun_out/ncu_$tag.txt 2>&1
+  ncu -i /tmp/ncu_$tag.ncu-rep --page raw --csv > gpurun_out/ncu_${tag}_raw.csv 2>&1
+  if [ "$SRC" = 1 ]; then ncu -i /tmp/ncu_$tag.ncu-rep --page source --csv --print-source sass > gpurun_out/ncu_${tag}_sass.csv 2>&1; fi
+  rm -f /tmp/ncu_$tag.ncu-rep
+}
+SRC=1 cap c5 --config C5 --frames 16384
+SRC=1 cap c2 --config C2 --ebn0 1.0
+cap c3r12 --config C3-R1/2
+SRC=1 cap c4 --frames 32768
+cap t1r14 --config T1-R1/4 --frames 1000
