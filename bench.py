@@ -737,6 +737,7 @@ def main():
         }
         if len(results) > 1:
             line["points"] = [point_summary(wl, p, r, args.steps) for p, r in zip(points, results)]
+            line["sweep_fit"] = sweep_fit(wl, results, args.steps)
             line["config"]["ebn0_db"] = list(wl.ebn0_db)
             line["config"]["frame_seed"] = list(wl.frame_seeds)
             line["config"]["workload"] += f" (sweep {', '.join(str(x) for x in wl.ebn0_db)} dB)"
@@ -744,6 +745,35 @@ def main():
     if launched:
         dist.destroy_process_group()
     return 0
+
+
+def sweep_fit(wl, results, steps):
+    """Early-termination sweep (C2): a least-squares fit of decode time per
+    step against mean iterations over the points, t = a + b x iterations.
+    b is the cost of one iteration of every frame (its SFU-model fraction is
+    the decoder's per-iteration efficiency); a / b is the per-frame fixed cost
+    in iterations (ingest, output, the check phase that detects convergence
+    one phase late, the tail of the persistent grid) -- it is what pulls the
+    fraction down at high Eb/N0, where frames stop after 5-7 iterations."""
+    xs = [r["counters"][4] / max(r["counters"][5], 1) for r in results]
+    ys = [r["dec_ms"] / steps for r in results]
+    n = len(xs)
+    mx, my = sum(xs) / n, sum(ys) / n
+    sxx = sum((x - mx) ** 2 for x in xs)
+    if sxx <= 0:
+        return None
+    b = sum((x - mx) * (y - my) for x, y in zip(xs, ys)) / sxx
+    a = my - b * mx
+    frames = results[0]["counters"][5]
+    peak = results[0]["roofline"].get("sfu_model", results[0]["roofline"])["peak"]
+    per_iter = frames * wl.edges / (b / 1e3) / 1e9 if b > 0 else None
+    return {"decode_ms_per_iteration_of_all_frames": b, "decode_ms_fixed_per_step": a,
+            "fixed_cost_in_iterations_per_frame": a / b if b > 0 else None,
+            "per_iteration_gedge_updates_per_s": per_iter,
+            "per_iteration_sfu_frac": per_iter / peak if per_iter else None,
+            "note": "decode time = fixed + per-iteration x mean iterations, fitted over the sweep; at high Eb/N0 "
+                    "the fixed per-frame cost weighs on few iterations, so the fraction on executed iterations "
+                    "falls below the per-iteration efficiency"}
 
 
 def point_summary(wl, p, r, steps):

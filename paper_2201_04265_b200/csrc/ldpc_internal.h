@@ -144,7 +144,8 @@ inline bool band_frame_fits_sm(int32_t n, int32_t wc) { return size_t(wc) * size
 // Two-slot exchange kernel (xband2_kernel): four regions + shared tables.
 inline size_t xband2_smem_bytes(int32_t n, int32_t wc, int32_t wr, int32_t C, int32_t cap) {
     const size_t nq = size_t(n / wr / C) * size_t(wr);
-    return 4 * size_t(cap) * 4 + 2 * size_t(wc - 1) * nq * 2 + 16 + 2 * 8 * (3 + size_t(wc - 1)) + 2 * 4 * size_t(C);
+    // four regions + the two slot tables as 32-bit offsets + barriers, flags
+    return 4 * size_t(cap) * 4 + 2 * size_t(wc - 1) * nq * 4 + 16 + 2 * 8 * (3 + size_t(wc - 1)) + 2 * 4 * size_t(C);
 }
 // Frames larger than one SM whose 16-CTA view fits two frames per CTA with one
 // row per thread use 16-CTA clusters and two frames in flight (the (3,6)
@@ -305,7 +306,7 @@ struct XClusterPlan {
 bool xcluster_plan(const ldpc_code &c, int64_t frames, bool et, XClusterPlan &p);
 ldpc_status xcluster_launch(const ldpc_code &c, const XClusterPlan &p, const float *llr, int64_t frames,
                             const ldpc_decode_opts &o, uint32_t *bits, uint8_t *syn, int32_t *iters, float *post,
-                            void *stream);
+                            void *ws, size_t ws_bytes, void *stream);
 ldpc_status cluster_launch(const ldpc_code &c, const ClusterPlan &p, const float *llr, int64_t frames,
                            const ldpc_decode_opts &o, uint32_t *bits, uint8_t *syn, int32_t *iters, float *post,
                            void *ws, size_t ws_bytes, void *stream);

@@ -126,12 +126,34 @@ __device__ __forceinline__ void ld_u16_row(const uint16_t *p, uint32_t (&o)[D]) 
     }
 }
 
+template <int D>
+__device__ __forceinline__ void ld_u32_row(const uint32_t *p, uint32_t (&o)[D]) {
+    // D 32-bit slots from shared memory; p is 16-byte aligned for D % 4 == 0, 8-byte for D even
+    if constexpr (D % 4 == 0) {
+#pragma unroll
+        for (int w = 0; w < D / 4; ++w) {
+            const uint4 x = reinterpret_cast<const uint4 *>(p)[w];
+            o[4 * w] = x.x; o[4 * w + 1] = x.y; o[4 * w + 2] = x.z; o[4 * w + 3] = x.w;
+        }
+    } else if constexpr (D % 2 == 0) {
+#pragma unroll
+        for (int w = 0; w < D / 2; ++w) {
+            const uint2 x = reinterpret_cast<const uint2 *>(p)[w];
+            o[2 * w] = x.x; o[2 * w + 1] = x.y;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < D; ++j) o[j] = p[j];
+    }
+}
+
 struct XArgs {
     DeviceCode code;
     const float *llr;
     int64_t frames;
     int32_t max_iter;
     int32_t adapt_votes;    // xband2: psi votes only after a hit (or every 4th iteration)
+    float *rws;             // xband2: R' = clamp(R) log2(e) per (cluster, slot, variable), written at V-phase 0
     uint32_t *bits;
     uint8_t *syn_ok;
     int32_t *iters;
@@ -447,9 +469,11 @@ __global__ void __launch_bounds__(MAXT, 1) xband2_kernel(const XArgs a) {
     const int64_t cid = cluster_id_x(), ncl = ncluster_x();
     char *varr[2] = {smem, smem + 2 * cap_b};
     char *rowr[2] = {smem + cap_b, smem + 3 * cap_b};
-    uint16_t *vtab = reinterpret_cast<uint16_t *>(smem + 4 * cap_b);
-    uint16_t *rtab = vtab + size_t(nq) * NB;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + ((4 * cap_b + 4u * uint32_t(NB * nq) + 15u) & ~15u));
+    // slot tables widened to 32-bit byte offsets in shared memory (vector
+    // loads, no unpacking in the phases)
+    uint32_t *vtab = reinterpret_cast<uint32_t *>(smem + 4 * cap_b);
+    uint32_t *rtab = vtab + size_t(nq) * NB;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + ((4 * cap_b + 8u * uint32_t(NB * nq) + 15u) & ~15u));
     constexpr int NBAR = 2 + H + NC;                 // per slot: var, row, vchunk, cchunk[NC]
     int *flags = reinterpret_cast<int *>(bars + 2 * NBAR);   // [2][C]
     const uint32_t bar0 = saddr(bars);
@@ -460,14 +484,20 @@ __global__ void __launch_bounds__(MAXT, 1) xband2_kernel(const XArgs a) {
     const int nkey = C * C * H * NC;
     const int32_t *varOff = code.xband_seg, *rowOff = code.xband_seg + nkey, *sbytes = code.xband_seg + 2 * nkey;
     auto key = [](int s, int d, int h, int c) { return ((s * C + d) * H + h) * NC + c; };
+    auto rslot = [&](int sl) { return a.rws + (size_t(cid) * 2 + size_t(sl)) * size_t(n); };
     {
         const uint32_t *src = reinterpret_cast<const uint32_t *>(code.xband_sidx + size_t(q) * nq * NB);
-        uint32_t *dst = reinterpret_cast<uint32_t *>(vtab);
-        for (int i = tt; i < nq * NB / 2; i += blockDim.x) dst[i] = __ldg(src + i);
+        for (int i = tt; i < nq * NB / 2; i += blockDim.x) {
+            const uint32_t x = __ldg(src + i);
+            reinterpret_cast<uint2 *>(vtab)[i] = make_uint2(x & 0xffffu, x >> 16);
+        }
         for (int b = 0; b < NB; ++b) {
             const uint32_t *rs = reinterpret_cast<const uint32_t *>(code.xband_ridx + size_t(b) * n + size_t(q) * mbq * WR);
-            uint32_t *rd = reinterpret_cast<uint32_t *>(rtab + size_t(b) * mbq * WR);
-            for (int i = tt; i < mbq * WR / 2; i += blockDim.x) rd[i] = __ldg(rs + i);
+            uint2 *rd = reinterpret_cast<uint2 *>(rtab + size_t(b) * mbq * WR);
+            for (int i = tt; i < mbq * WR / 2; i += blockDim.x) {
+                const uint32_t x = __ldg(rs + i);
+                rd[i] = make_uint2(x & 0xffffu, x >> 16);
+            }
         }
     }
     uint32_t rx_l = 0, rx_e = 0;
@@ -565,7 +595,9 @@ __global__ void __launch_bounds__(MAXT, 1) xband2_kernel(const XArgs a) {
                         lds_row<WR>(reinterpret_cast<const char *>(a.llr + fs[sl] * int64_t(n)), uint32_t(v0) * 4u, lv);
 #pragma unroll
                         for (int j = 0; j < WR; ++j) lv[j] = fminf(fmaxf(lv[j], -30.0f), 30.0f) * kL2E;
-                        const uint16_t *vt = vtab + size_t(r) * WR * NB;
+                        // R' of the slot's frame, reread by every V-phase (L2-resident workspace)
+                        sts_row<WR>(reinterpret_cast<char *>(rslot(sl)), uint32_t(v0) * 4u, lv);
+                        const uint32_t *vt = vtab + size_t(r) * WR * NB;
 #pragma unroll
                         for (int j = 0; j < WR; ++j)
 #pragma unroll
@@ -588,10 +620,8 @@ __global__ void __launch_bounds__(MAXT, 1) xband2_kernel(const XArgs a) {
 #pragma unroll
                         for (int b = 0; b < NB; ++b) {
                             if (r < mbq) {
-                                const uint16_t *rt = rtab + (size_t(b) * mbq + r) * WR;
                                 uint32_t s_[WR];
-#pragma unroll
-                                for (int j = 0; j < WR; ++j) s_[j] = rt[j];
+                                ld_u32_row<WR>(rtab + (size_t(b) * mbq + r) * WR, s_);
                                 float x[WR], e[WR];
 #pragma unroll
                                 for (int j = 0; j < WR; ++j) x[j] = *reinterpret_cast<const float *>(rowr[sl] + s_[j]);
@@ -610,18 +640,15 @@ __global__ void __launch_bounds__(MAXT, 1) xband2_kernel(const XArgs a) {
                     if (sl < ns) {
                         float lv[WR];
                         if (own)
-                            lds_row<WR>(reinterpret_cast<const char *>(a.llr + fs[sl] * int64_t(n)),
-                                        uint32_t((int(q) * mbq + r) * WR) * 4u, lv);
+                            lds_row<WR>(reinterpret_cast<const char *>(rslot(sl)), uint32_t((int(q) * mbq + r) * WR) * 4u, lv);
                         wait_var(sl);
                         if (own) {
-                            const uint16_t *vt = vtab + size_t(r) * WR * NB;
                             uint32_t s_[WR * NB];
-#pragma unroll
-                            for (int i = 0; i < WR * NB; ++i) s_[i] = vt[i];
+                            ld_u32_row<WR * NB>(vtab + size_t(r) * WR * NB, s_);
                             float eb[WR * NB];
 #pragma unroll
                             for (int j = 0; j < WR; ++j) {
-                                lv[j] = fminf(fmaxf(lv[j], -30.0f), 30.0f) * kL2E + e0[sl][j];
+                                lv[j] += e0[sl][j];
 #pragma unroll
                                 for (int b = 0; b < NB; ++b) {
                                     eb[j * NB + b] = *reinterpret_cast<const float *>(varr[sl] + s_[j * NB + b]);
@@ -658,7 +685,7 @@ __global__ void __launch_bounds__(MAXT, 1) xband2_kernel(const XArgs a) {
                 if (sl < ns) {
                     wait_row(sl);
                     for (int rr = tt; rr < NB * mbq; rr += TW) {
-                        const uint16_t *rt = rtab + size_t(rr) * WR;
+                        const uint32_t *rt = rtab + size_t(rr) * WR;
                         uint32_t rp = 0;
 #pragma unroll
                         for (int j = 0; j < WR; ++j) rp ^= (*reinterpret_cast<const float *>(rowr[sl] + rt[j]) >= 0.0f) ? 1u : 0u;
@@ -681,7 +708,7 @@ __global__ void __launch_bounds__(MAXT, 1) xband2_kernel(const XArgs a) {
             const int w_lo = (int(q) * nq + 31) / 32;
             const int w_hi = (int(q) == C - 1) ? nw : ((int(q) + 1) * nq + 31) / 32;
             const int qn = (int(q) + 1 < C) ? int(q) + 1 : int(q);
-            const uint16_t *tnext = cg::this_cluster().map_shared_rank(vtab, qn);
+            const uint32_t *tnext = cg::this_cluster().map_shared_rank(vtab, qn);
             for (int sl = 0; sl < ns; ++sl) {
                 const char *vnext = cg::this_cluster().map_shared_rank(varr[sl], qn);
                 uint32_t *bits = a.bits + fs[sl] * int64_t(nw);
@@ -776,7 +803,7 @@ bool xcluster_plan(const ldpc_code &c, int64_t frames, bool et, XClusterPlan &p)
                     p.capacity = 2 * int64_t(ncl);
                     ncl = int(std::min<int64_t>(ncl, (frames + 1) / 2));
                     p.grid = ncl * C;
-                    p.ws_bytes = 0;
+                    p.ws_bytes = size_t(ncl) * 2 * size_t(c.n) * 4;     // R' per (cluster, slot)
                     return true;
                 }
             }
@@ -804,13 +831,15 @@ bool xcluster_plan(const ldpc_code &c, int64_t frames, bool et, XClusterPlan &p)
 
 ldpc_status xcluster_launch(const ldpc_code &c, const XClusterPlan &p, const float *llr, int64_t frames,
                             const ldpc_decode_opts &o, uint32_t *bits, uint8_t *syn, int32_t *iters, float *post,
-                            void *stream) {
+                            void *ws, size_t ws_bytes, void *stream) {
+    if (p.ws_bytes > 0 && (!ws || ws_bytes < p.ws_bytes)) return LDPC_ERR_ARG;
     XArgs a;
     a.code = c.dev;
     a.llr = llr;
     a.frames = frames;
     a.max_iter = o.max_iter;
     a.adapt_votes = std::getenv("LDPC_XVOTE_ALWAYS") ? 0 : 1;
+    a.rws = static_cast<float *>(ws);
     a.bits = bits;
     a.syn_ok = syn;
     a.iters = iters;

@@ -614,7 +614,7 @@ ldpc_status ldpc_decode(const ldpc_code *code, const float *d_llr, int64_t frame
                                      d_ws, ws_bytes, stream);
         case 7:
             return ldpc::xcluster_launch(*code, r.x, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters,
-                                         d_posterior, stream);
+                                         d_posterior, d_ws, ws_bytes, stream);
         case 8:
             return ldpc::edge_launch(*code, r.edge, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters, d_posterior,
                                      stream);
