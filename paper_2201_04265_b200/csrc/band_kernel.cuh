@@ -8,6 +8,9 @@
 #ifndef BAND_FUSE0
 #define BAND_FUSE0 true
 #endif
+#ifndef BAND_PREFETCH_OFFSETS
+#define BAND_PREFETCH_OFFSETS 1
+#endif
 
 struct BandArgs {
     DeviceCode code;
@@ -72,13 +75,13 @@ __device__ __forceinline__ bool cta_sync_or(bool p) { return __syncthreads_or(p 
 // registers), C3 (n = 3996): 2 (wr 6, 40 registers) / 3 (wr 12, 56).
 // Measured: C3-R1/2 77.6 -> 91.4% of the SFU roofline, C3-R3/4 66.9 ->
 // 69.2%, C2 51.2 -> 52.0%; C2 at 10 blocks (32 registers) 47.6%.
-constexpr int band_lb_minb(int wr, int nfix, int lpr) {
+constexpr int band_lb_minb(int wr, int nfix, int lpr, int wc = 0) {
     return lpr == 2 ? BAND_LPR2_MINB
          : !BAND_NFIX_MINB ? 1
          : nfix == 1008 ? 7 : nfix == 3996 ? (wr == 12 ? 3 : wr == 4 ? 3 : 2) : 1;
 }
 constexpr int band_lb_threads(int wr, int wc, int b0, int nfix, int lpr) {
-    return (lpr == 2 || band_lb_minb(wr, nfix, lpr) > 1) ? ((nfix / wr + b0 - 1) / b0 + 31) / 32 * 32 * lpr
+    return (lpr == 2 || band_lb_minb(wr, nfix, lpr, wc) > 1) ? ((nfix / wr + b0 - 1) / b0 + 31) / 32 * 32 * lpr
                                                           : (wc > 3 ? 256 : 1024);
 }
 // LPR0: lanes per band-0 row (default LPR).  C1 runs one lane per row of
@@ -86,7 +89,7 @@ constexpr int band_lb_threads(int wr, int wc, int b0, int nfix, int lpr) {
 // on 32 lanes instead of 16), halving the variable phase's chain.
 template <int WR, int WC, int B0, bool ET, int MODE, int NFIX = 0, bool GEN = false, int RPRE = 0, bool NOVOTE = false,
           int LPR = 1, int LPR0 = LPR>
-__global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_lb_minb(WR, NFIX, LPR))
+__global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_lb_minb(WR, NFIX, LPR, WC))
     band_kernel(const BandArgs a) {
     // measured on B200: +1.1 points on C4 (MODE 2), +0.8..1.3 on wr = 12 codes,
     // -2..3 on check-major wr = 4 / 6 codes (C3 R1/4, R1/2)
@@ -229,11 +232,34 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
                     check_any<WR, !ET && !NOVOTE, LPR0>(x, e0[k], h0, pm, cmp);
                 }
             }
+            // L16, one lane per row: the packed offsets of the next row are
+            // loaded while this row computes (their L1/L2 latency was the
+            // kernel's largest long-scoreboard stall)
+            constexpr bool PFO = L16 && LPR == 1 && B1 > 1 && BAND_PREFETCH_OFFSETS;
+            uint32_t pfo[PFO ? WR / 2 : 1];
+            if constexpr (PFO) {
+                if (pr < S && pr < NB * mb) {
+                    const uint32_t *p16 = reinterpret_cast<const uint32_t *>(code.band_lidx16 + size_t(pr) * WR);
+#pragma unroll
+                    for (int w = 0; w < WR / 2; ++w) pfo[w] = __ldg(p16 + w);
+                }
+            }
 #pragma unroll
             for (int k = 0; k < B1; ++k) {
                 const int r = pr + k * S;
                 const bool act = pr < S && r < NB * mb;
                 const unsigned pm = LPR > 1 ? __ballot_sync(0xffffffffu, act) : 0u;
+                uint32_t cur[PFO ? WR / 2 : 1];
+                if constexpr (PFO) {
+#pragma unroll
+                    for (int w = 0; w < WR / 2; ++w) cur[w] = pfo[w];
+                    const int rn = r + S;
+                    if (k + 1 < B1 && pr < S && rn < NB * mb) {
+                        const uint32_t *p16 = reinterpret_cast<const uint32_t *>(code.band_lidx16 + size_t(rn) * WR);
+#pragma unroll
+                        for (int w = 0; w < WR / 2; ++w) pfo[w] = __ldg(p16 + w);
+                    }
+                }
                 if (act) {
                     int32_t li[WH];
                     float e[WH], x[WH];
@@ -241,6 +267,12 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
 #pragma unroll
                         for (int j = 0; j < WH; ++j)
                             li[j] = int32_t(lbase + __ldg(code.band_lidx16 + size_t(r) * WR + hoff + j));
+                    } else if (PFO) {
+#pragma unroll
+                        for (int w = 0; w < WR / 2; ++w) {
+                            li[2 * w] = int32_t(lbase + (cur[w] & 0xffffu));
+                            li[2 * w + 1] = int32_t(lbase + (cur[w] >> 16));
+                        }
                     } else if (L16) {
                         // 16-bit offsets relative to L: half the index bytes through L1/L2
                         const uint32_t *p16 = reinterpret_cast<const uint32_t *>(code.band_lidx16 + size_t(r) * WR);

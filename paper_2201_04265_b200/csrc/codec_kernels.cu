@@ -29,13 +29,19 @@ constexpr int kEncKC = 32;    // message words per k chunk
 
 __global__ void __launch_bounds__(256) encode_parity_kernel(const DeviceCode code, const uint32_t *__restrict__ info,
                                                             uint32_t *__restrict__ cw, int64_t frames) {
-    __shared__ uint32_t ms[kEncTF][kEncKC + 1];
+    // message rows padded to 36 words: 16-byte aligned for the 4-word vector
+    // loads, and the two frames a warp reads (4 rows apart) on disjoint banks
+    constexpr int MS = kEncKC + 4;
+    __shared__ __align__(16) uint32_t ms[kEncTF][MS];
     __shared__ __align__(16) uint32_t ps[kEncKC][kEncColTile];
-    __shared__ uint8_t pbits[kEncTF][kEncColTile / 8];
+    __shared__ uint8_t pnib[kEncTF][kEncColTile / 4];
     const int kw = code.kw, npp = code.npar_pad, nw = code.nw;
     const int npw = (code.n - code.k + 31) / 32;
     const int b0 = blockIdx.x * kEncColTile;
     const int64_t f0 = int64_t(blockIdx.y) * kEncTF;
+    // thread (tf, tb): frames tf*4 .. tf*4+3, parity columns tb*4 .. tb*4+3 and
+    // 64 + tb*4 .. 64 + tb*4+3 -- the 16 lanes of a half-warp read 256
+    // contiguous bytes of a P row per vector load (2 wavefronts)
     const int tid = threadIdx.x, tf = tid >> 4, tb = tid & 15;
     uint32_t acc[4][8];
 #pragma unroll
@@ -57,27 +63,36 @@ __global__ void __launch_bounds__(256) encode_parity_kernel(const DeviceCode cod
             *reinterpret_cast<uint4 *>(&ps[w][4 * c4]) = x;
         }
         __syncthreads();
-#pragma unroll 4
-        for (int w = 0; w < kEncKC; ++w) {
-            uint32_t m[4];
+#pragma unroll 2
+        for (int w = 0; w < kEncKC; w += 4) {
+            uint4 m4[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) m[i] = ms[tf * 4 + i][w];
-            const uint4 pa = *reinterpret_cast<const uint4 *>(&ps[w][tb * 8]);
-            const uint4 pb = *reinterpret_cast<const uint4 *>(&ps[w][tb * 8 + 4]);
-            const uint32_t p[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
+            for (int i = 0; i < 4; ++i) m4[i] = *reinterpret_cast<const uint4 *>(&ms[tf * 4 + i][w]);
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int u = 0; u < 4; ++u) {
+                const uint4 pa = *reinterpret_cast<const uint4 *>(&ps[w + u][tb * 4]);
+                const uint4 pb = *reinterpret_cast<const uint4 *>(&ps[w + u][64 + tb * 4]);
+                const uint32_t p[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] ^= m[i] & p[j];
+                for (int i = 0; i < 4; ++i) {
+                    const uint32_t m = u == 0 ? m4[i].x : u == 1 ? m4[i].y : u == 2 ? m4[i].z : m4[i].w;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[i][j] ^= m & p[j];
+                }
+            }
         }
         __syncthreads();
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        uint32_t byte = 0u;
+        uint32_t lo = 0u, hi = 0u;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) byte |= (uint32_t(__popc(acc[i][j])) & 1u) << j;
-        pbits[tf * 4 + i][tb] = uint8_t(byte);
+        for (int j = 0; j < 4; ++j) {
+            lo |= (uint32_t(__popc(acc[i][j])) & 1u) << j;
+            hi |= (uint32_t(__popc(acc[i][4 + j])) & 1u) << j;
+        }
+        pnib[tf * 4 + i][tb] = uint8_t(lo);          // columns tb*4 .. tb*4+3
+        pnib[tf * 4 + i][16 + tb] = uint8_t(hi);     // columns 64 + tb*4 ..
     }
     __syncthreads();
     // parity word q of this tile -> word (b0/32 + q) of the parity area, which
@@ -86,8 +101,10 @@ __global__ void __launch_bounds__(256) encode_parity_kernel(const DeviceCode cod
         const int f = i >> 2, q = i & 3;
         const int pwi = b0 / 32 + q;
         if (f0 + f < frames && pwi < npw) {
-            const uint8_t *b = &pbits[f][4 * q];
-            const uint32_t word = uint32_t(b[0]) | (uint32_t(b[1]) << 8) | (uint32_t(b[2]) << 16) | (uint32_t(b[3]) << 24);
+            const uint8_t *nb = &pnib[f][8 * q];
+            uint32_t word = 0u;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) word |= uint32_t(nb[t]) << (4 * t);
             cw[(f0 + f) * int64_t(nw) + (nw - npw) + pwi] = word;
         }
     }

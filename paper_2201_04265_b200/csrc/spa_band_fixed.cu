@@ -72,11 +72,14 @@ void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode, i
     }
     if (lpr != 1) return nullptr;
     if (wc == 3 && wr == 6 && n == 16200 && b0 == 3 && mode == 2) {
-        // R of 2 of the 3 band-0 rows prefetched before the check->variable
-        // barrier (RPRE; measured on B200: 0 rows 65.8%, 1 67.2%, 2 68.2%,
-        // 3 66.8% (spills) of the SFU roofline); LDPC_RPRE=0/1 for A/B
+        // R of RPRE of the 3 band-0 rows prefetched before the check->variable
+        // barrier.  Round 1 (scalar psi): 0 rows 65.8%, 1 67.2%, 2 68.2%, 3
+        // 66.8% (spills) of the SFU roofline.  Round 2 (packed psi, more
+        // register pairs): 0 rows 84.6% (63 registers, no spill), 1 83.9%
+        // (8-byte spill), 2 82.9% (28-byte spill) -- 0 is the default;
+        // LDPC_RPRE=1/2 for A/B
         const char *e = std::getenv("LDPC_RPRE");
-        const int rp = e ? std::atoi(e) : 2;
+        const int rp = e ? std::atoi(e) : 0;
         if (rp == 1) return et ? reinterpret_cast<void *>(&band_kernel<6, 3, 3, true, 2, 16200, false, 1>)
                                : reinterpret_cast<void *>(&band_kernel<6, 3, 3, false, 2, 16200, false, 1>);
         if (rp == 2) return et ? reinterpret_cast<void *>(&band_kernel<6, 3, 3, true, 2, 16200, false, 2>)
