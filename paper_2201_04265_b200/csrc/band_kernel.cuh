@@ -8,9 +8,6 @@
 #ifndef BAND_FUSE0
 #define BAND_FUSE0 true
 #endif
-#ifndef BAND_PREFETCH_OFFSETS
-#define BAND_PREFETCH_OFFSETS 1
-#endif
 
 struct BandArgs {
     DeviceCode code;
@@ -232,34 +229,11 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
                     check_any<WR, !ET && !NOVOTE, LPR0>(x, e0[k], h0, pm, cmp);
                 }
             }
-            // L16, one lane per row: the packed offsets of the next row are
-            // loaded while this row computes (their L1/L2 latency was the
-            // kernel's largest long-scoreboard stall)
-            constexpr bool PFO = L16 && LPR == 1 && B1 > 1 && BAND_PREFETCH_OFFSETS;
-            uint32_t pfo[PFO ? WR / 2 : 1];
-            if constexpr (PFO) {
-                if (pr < S && pr < NB * mb) {
-                    const uint32_t *p16 = reinterpret_cast<const uint32_t *>(code.band_lidx16 + size_t(pr) * WR);
-#pragma unroll
-                    for (int w = 0; w < WR / 2; ++w) pfo[w] = __ldg(p16 + w);
-                }
-            }
 #pragma unroll
             for (int k = 0; k < B1; ++k) {
                 const int r = pr + k * S;
                 const bool act = pr < S && r < NB * mb;
                 const unsigned pm = LPR > 1 ? __ballot_sync(0xffffffffu, act) : 0u;
-                uint32_t cur[PFO ? WR / 2 : 1];
-                if constexpr (PFO) {
-#pragma unroll
-                    for (int w = 0; w < WR / 2; ++w) cur[w] = pfo[w];
-                    const int rn = r + S;
-                    if (k + 1 < B1 && pr < S && rn < NB * mb) {
-                        const uint32_t *p16 = reinterpret_cast<const uint32_t *>(code.band_lidx16 + size_t(rn) * WR);
-#pragma unroll
-                        for (int w = 0; w < WR / 2; ++w) pfo[w] = __ldg(p16 + w);
-                    }
-                }
                 if (act) {
                     int32_t li[WH];
                     float e[WH], x[WH];
@@ -267,12 +241,6 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
 #pragma unroll
                         for (int j = 0; j < WH; ++j)
                             li[j] = int32_t(lbase + __ldg(code.band_lidx16 + size_t(r) * WR + hoff + j));
-                    } else if (PFO) {
-#pragma unroll
-                        for (int w = 0; w < WR / 2; ++w) {
-                            li[2 * w] = int32_t(lbase + (cur[w] & 0xffffu));
-                            li[2 * w + 1] = int32_t(lbase + (cur[w] >> 16));
-                        }
                     } else if (L16) {
                         // 16-bit offsets relative to L: half the index bytes through L1/L2
                         const uint32_t *p16 = reinterpret_cast<const uint32_t *>(code.band_lidx16 + size_t(r) * WR);
