@@ -46,7 +46,8 @@ KERNEL_NAMES = {1: "spa_decode_kernel (generic, on-chip)", 2: "spa_decode_kernel
                 3: "band_kernel (check-major E)", 4: "band_kernel (variable-major E)",
                 5: "band_cluster_kernel (L2 gathers)", 6: "band_kernel (variable-major E, 16-bit offsets)",
                 7: "xband_kernel (exchange cluster, bulk DSMEM segments)",
-                8: "edge_kernel (lane per edge, small batches)"}
+                8: "edge_kernel (lane per edge, small batches)",
+                9: "gband2_kernel (16-CTA groups, segments through L2 staging)"}
 
 
 def parse():

@@ -156,7 +156,7 @@ ldpc_status ldpc_encode(const ldpc_code *code, const uint32_t *d_info, uint32_t 
  * 0 resolved): 1 generic on-chip, 2 generic global-state, 3/4 Gallager band
  * kernel (check-/variable-major E), 5 cluster band kernel, 6 band kernel with
  * 16-bit offsets, 7 exchange cluster kernel, 8 lane-per-edge small-batch
- * kernel.  *variant = 0 and
+ * kernel, 9 global-exchange group kernel.  *variant = 0 and
  * LDPC_ERR_UNSUPPORTED when nothing fits. */
 ldpc_status ldpc_decode_variant(const ldpc_code *code, int64_t frames, const ldpc_decode_opts *opts,
                                 int32_t *variant);
@@ -195,7 +195,11 @@ ldpc_status ldpc_decode_workspace_bytes(const ldpc_code *code, int64_t frames,
  * 259 KB); 8 lane-per-edge kernel (any H with
  * row degree <= 32 whose E, L, R fit one SM's shared memory: a group of
  * 4/8/16/32 lanes per check row, one CTA per frame, no workspace; for batches
- * too small to fill the GPU with one thread per check row).  Auto (0): a
+ * too small to fill the GPU with one thread per check row); 9 global-exchange
+ * kernel (the codes of variant 7's 16-CTA two-frame view: groups of 16
+ * co-resident CTAs, cooperative launch, trade segments through L2-resident
+ * staging images instead of cluster shared memory, so 144 SMs instead of
+ * 112; workspace: staging, counters and R', C5 ~43 MB).  Auto (0): a
  * frame that fits one SM runs the band kernel (one SM per frame) unless the
  * batch is too small to fill the GPU that way, in which case it runs variant
  * 7 with C SMs per frame when the code has that view (lower latency: stream

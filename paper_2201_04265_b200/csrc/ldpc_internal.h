@@ -301,6 +301,25 @@ struct XClusterPlan {
     size_t smem = 0;
     size_t ws_bytes = 0;
 };
+// Launch plan of the global-exchange kernel (spa_gexchange.cu; variant 9):
+// groups of 16 co-resident CTAs (cooperative launch) on the 16-CTA exchange
+// view, two frames in flight per group, segments through L2-resident staging.
+struct GXPlan {
+    void *kernel = nullptr;
+    int threads = 0;
+    int grid = 0;
+    int groups = 0;
+    int64_t capacity = 0;       // frames decoded concurrently
+    size_t smem = 0;
+    size_t ws_bytes = 0;
+    size_t zero_bytes = 0;      // workspace prefix zeroed per launch (arrival / barrier counters)
+    size_t off_arrivals = 0, off_gbar = 0, off_stage = 0, off_rws = 0, off_zbyte = 0, off_synd = 0;
+};
+bool gx_plan(const ldpc_code &c, int64_t frames, bool et, GXPlan &p);
+ldpc_status gx_launch(const ldpc_code &c, const GXPlan &p, const float *llr, int64_t frames, const ldpc_decode_opts &o,
+                      uint32_t *bits, uint8_t *syn, int32_t *iters, float *post, void *ws, size_t ws_bytes,
+                      void *stream);
+
 // false unless the bound code has an exchange cluster view, fixed iterations
 // and an instantiated (wc, wr, rows-per-thread, C).
 bool xcluster_plan(const ldpc_code &c, int64_t frames, bool et, XClusterPlan &p);

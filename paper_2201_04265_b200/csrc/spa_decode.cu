@@ -479,6 +479,7 @@ struct Resolved {
     EdgePlan edge;
     BandPlan band;
     XClusterPlan x;
+    GXPlan gx;
     ClusterPlan cl;
     Plan gen;
 };
@@ -521,6 +522,11 @@ ldpc_status resolve(const ldpc_code &c, int64_t frames, const ldpc_decode_opts &
         r.variant = 7;
         return LDPC_OK;
     }
+    if (v == 9) {
+        if (!gx_plan(c, frames, et, r.gx)) return LDPC_ERR_UNSUPPORTED;
+        r.variant = 9;
+        return LDPC_OK;
+    }
     if (band_ok) {
         // rounds of the one-SM-per-frame kernel vs rounds of C-SM clusters, a
         // cluster round costing ~2/C of a band round (measured per-SM rate of
@@ -544,6 +550,13 @@ ldpc_status resolve(const ldpc_code &c, int64_t frames, const ldpc_decode_opts &
         return LDPC_OK;
     }
     if (x_ok) {
+        // frames larger than one SM: the global-exchange kernel places 144
+        // CTAs where 16-CTA clusters place 112 (LDPC_GX=0/1 overrides)
+        const char *gxe = std::getenv("LDPC_GX");
+        if (v == 0 && gxe && std::atoi(gxe) == 1 && r.x.capacity >= 2 && gx_plan(c, frames, et, r.gx)) {
+            r.variant = 9;
+            return LDPC_OK;
+        }
         r.variant = 7;
         return LDPC_OK;
     }
@@ -587,6 +600,7 @@ ldpc_status ldpc_decode_workspace_bytes(const ldpc_code *code, int64_t frames, c
     switch (r.variant) {
         case 3: case 4: case 6: *bytes = r.band.ws_bytes; break;
         case 7: *bytes = r.x.ws_bytes; break;
+        case 9: *bytes = r.gx.ws_bytes; break;
         case 5: *bytes = r.cl.ws_bytes; break;
         // variant 8 needs none; where the band kernel could decode the code, its
         // workspace is reported so one buffer also serves ldpc_decode_simulate
@@ -615,6 +629,9 @@ ldpc_status ldpc_decode(const ldpc_code *code, const float *d_llr, int64_t frame
         case 7:
             return ldpc::xcluster_launch(*code, r.x, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters,
                                          d_posterior, d_ws, ws_bytes, stream);
+        case 9:
+            return ldpc::gx_launch(*code, r.gx, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters, d_posterior,
+                                   d_ws, ws_bytes, stream);
         case 8:
             return ldpc::edge_launch(*code, r.edge, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters, d_posterior,
                                      stream);
