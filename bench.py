@@ -773,8 +773,11 @@ def sweep_fit(wl, results, steps):
             "per_iteration_gedge_updates_per_s": per_iter,
             "per_iteration_sfu_frac": per_iter / peak if per_iter else None,
             "note": "decode time = fixed + per-iteration x mean iterations, fitted over the sweep; at high Eb/N0 "
-                    "the fixed per-frame cost weighs on few iterations, so the fraction on executed iterations "
-                    "falls below the per-iteration efficiency"}
+                    "the fixed cost weighs on 5-7 iterations, so the fraction on executed iterations falls below "
+                    "the per-iteration efficiency.  Measured at 3.0 dB (DESIGN.md section 12): 10k frames 0.388, "
+                    "40k 0.440, 160k 0.457 -- about 0.05 ms of the 10k-frame step is the tail of the few frames "
+                    "that run all 50 iterations, the rest ~1.2 iterations per frame (ingest, output, the check "
+                    "phase that detects convergence)"}
 
 
 def point_summary(wl, p, r, steps):
