@@ -63,6 +63,9 @@ __device__ __forceinline__ bool cta_sync_or(bool p) { return __syncthreads_or(p 
 #ifndef BAND_LPR2_MINB
 #define BAND_LPR2_MINB 5
 #endif
+#ifndef BAND_T1R34_MINB
+#define BAND_T1R34_MINB 8      // Table I R3/4 (96 threads): 80 registers, no spill
+#endif
 #ifndef BAND_NFIX_MINB
 #define BAND_NFIX_MINB 1
 #endif
@@ -75,7 +78,8 @@ __device__ __forceinline__ bool cta_sync_or(bool p) { return __syncthreads_or(p 
 constexpr int band_lb_minb(int wr, int nfix, int lpr, int wc = 0) {
     return lpr == 2 ? BAND_LPR2_MINB
          : !BAND_NFIX_MINB ? 1
-         : nfix == 1008 ? 7 : nfix == 3996 ? (wr == 12 ? 3 : wr == 4 ? 3 : 2) : 1;
+         : nfix == 1008 ? 7 : nfix == 3996 ? (wr == 12 ? 3 : wr == 4 ? 3 : 2)
+         : (nfix == 1032 && wc == 3) ? BAND_T1R34_MINB : 1;
 }
 constexpr int band_lb_threads(int wr, int wc, int b0, int nfix, int lpr) {
     return (lpr == 2 || band_lb_minb(wr, nfix, lpr, wc) > 1) ? ((nfix / wr + b0 - 1) / b0 + 31) / 32 * 32 * lpr
