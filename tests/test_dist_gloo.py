@@ -119,3 +119,20 @@ def test_shard_helpers():
     # C5 at N = 8: 125,000 frames per rank, 8 chunks (7 x 16384 + 10312)
     f0, c = bench.rank_share(1000000, 7, 8, "strong")
     assert (f0, c) == (875000, 125000) and len(bench.chunk_spans(f0, c, 16384)) == 8
+
+
+def test_sweep_fit_recovers_line():
+    """bench.sweep_fit (the C2 sweep's fixed + per-iteration decode-time fit)
+    recovers a known line t = a + b x iterations exactly."""
+    import bench
+    import ldpc_workloads as W
+    a, b = 0.14, 0.046
+    iters = [42.1, 23.2, 11.0, 6.9, 5.2]
+    frames = 10000
+    res = [{"counters": [0, 0, 0, 0, int(round(x * frames)), frames], "dec_ms": (a + b * (round(x * frames) / frames)) * 3,
+            "roofline": {"peak": 1163.28, "frac": 0.5}} for x in iters]
+    fit = bench.sweep_fit(W.C2, res, 3)
+    assert abs(fit["decode_ms_per_iteration_of_all_frames"] - b) < 1e-9
+    assert abs(fit["decode_ms_fixed_per_step"] - a) < 1e-9
+    assert abs(fit["fixed_cost_in_iterations_per_frame"] - a / b) < 1e-6
+    assert abs(fit["per_iteration_gedge_updates_per_s"] - frames * W.C2.edges / (b / 1e3) / 1e9) < 1e-6
