@@ -8,6 +8,9 @@
 #ifndef BAND_FUSE0
 #define BAND_FUSE0 true
 #endif
+#ifndef BAND_TMEM_OFFSETS
+#define BAND_TMEM_OFFSETS 1
+#endif
 
 struct BandArgs {
     DeviceCode code;
@@ -145,6 +148,43 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
 
     unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};       // GEN: this CTA's counters (thread 0)
     __shared__ int s_err[2];
+    // TMIDX (C4: n = 16200, 16-bit offsets, one lane per row): the packed L
+    // offsets of this thread's B1 rows of bands >= 1 are constant for the
+    // whole launch.  They live in Tensor Memory (256 columns, otherwise idle
+    // here) instead of being re-read through L1/L2 every iteration: warp w
+    // owns lanes 32 (w % 4) .. + 31 and columns 4 B1 (w / 4) ..; row k's three
+    // words sit at column 4 k of that range (tcgen05.ld, 12-cycle latency).
+    constexpr bool TMIDX = L16 && LPR == 1 && NFIX == 16200 && !GEN && WR == 6 && BAND_TMEM_OFFSETS;
+    __shared__ uint32_t s_tmem;
+    uint32_t tm_row0 = 0;
+    if constexpr (TMIDX) {
+        static_assert(4 * B1 * ((TFIX / 32 + 3) / 4) <= 256, "TMEM columns");
+        const uint32_t warp = uint32_t(tt) >> 5;
+        if (warp == 0) {
+            const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&s_tmem));
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(dst) : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        tm_row0 = s_tmem + ((32u * (warp & 3u)) << 16) + 4u * uint32_t(B1) * (warp >> 2);
+#pragma unroll
+        for (int k = 0; k < B1; ++k) {
+            const int r = pr + k * S;
+            uint32_t w0 = 0, w1 = 0, w2 = 0;
+            if (pr < S && r < NB * mb) {
+                const uint32_t *p16 = reinterpret_cast<const uint32_t *>(code.band_lidx16 + size_t(r) * WR);
+                w0 = __ldg(p16);
+                w1 = __ldg(p16 + 1);
+                w2 = __ldg(p16 + 2);
+            }
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(tm_row0 + 4u * k), "r"(w0),
+                         "r"(w1), "r"(w2), "r"(0u)
+                         : "memory");
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
     for (;;) {
         if (tt == 0) s_frame = (long long)atomicAdd(a.frame_counter, 1ull);
         if (GEN && tt < 2) s_err[tt] = 0;
@@ -238,10 +278,24 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
                 const int r = pr + k * S;
                 const bool act = pr < S && r < NB * mb;
                 const unsigned pm = LPR > 1 ? __ballot_sync(0xffffffffu, act) : 0u;
+                uint32_t tmw[TMIDX ? 4 : 1];
+                if constexpr (TMIDX) {
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(tmw[0]), "=r"(tmw[1]), "=r"(tmw[2]), "=r"(tmw[3])
+                                 : "r"(tm_row0 + 4u * k)
+                                 : "memory");
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                }
                 if (act) {
                     int32_t li[WH];
                     float e[WH], x[WH];
-                    if (L16 && LPR > 1) {
+                    if constexpr (TMIDX) {
+#pragma unroll
+                        for (int w = 0; w < WR / 2; ++w) {
+                            li[2 * w] = int32_t(lbase + (tmw[w] & 0xffffu));
+                            li[2 * w + 1] = int32_t(lbase + (tmw[w] >> 16));
+                        }
+                    } else if (L16 && LPR > 1) {
 #pragma unroll
                         for (int j = 0; j < WH; ++j)
                             li[j] = int32_t(lbase + __ldg(code.band_lidx16 + size_t(r) * WR + hoff + j));
@@ -427,5 +481,12 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
     if (GEN && tt == 0)
         for (int i = 0; i < 6; ++i)
             if (cnt[i]) atomicAdd(a.counters + i, cnt[i]);
+    if constexpr (TMIDX) {
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if ((tt >> 5) == 0)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(s_tmem) : "memory");
+    }
 }
 
