@@ -155,20 +155,24 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
     // owns lanes 32 (w % 4) .. + 31 and columns 4 B1 (w / 4) ..; row k's three
     // words sit at column 4 k of that range (tcgen05.ld, 12-cycle latency).
     constexpr bool TMIDX = L16 && LPR == 1 && NFIX == 16200 && !GEN && WR == 6 && BAND_TMEM_OFFSETS;
+    // ... and columns 256 + 8 B0 (w / 4) ..: the R' of this thread's band-0
+    // rows (row k at + 8 k), copied from L = R' at each frame's ingest and
+    // read by every variable phase (it lived in an L2-resident slot)
     __shared__ uint32_t s_tmem;
-    uint32_t tm_row0 = 0;
+    uint32_t tm_row0 = 0, tm_r0 = 0;
     if constexpr (TMIDX) {
-        static_assert(4 * B1 * ((TFIX / 32 + 3) / 4) <= 256, "TMEM columns");
+        static_assert(4 * B1 * ((TFIX / 32 + 3) / 4) <= 256 && 8 * B0 * ((TFIX / 32 + 3) / 4) <= 256, "TMEM columns");
         const uint32_t warp = uint32_t(tt) >> 5;
         if (warp == 0) {
             const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&s_tmem));
-            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(dst) : "memory");
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(dst) : "memory");
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         tm_row0 = s_tmem + ((32u * (warp & 3u)) << 16) + 4u * uint32_t(B1) * (warp >> 2);
+        tm_r0 = s_tmem + ((32u * (warp & 3u)) << 16) + 256u + 8u * uint32_t(B0) * (warp >> 2);
 #pragma unroll
         for (int k = 0; k < B1; ++k) {
             const int r = pr + k * S;
@@ -217,7 +221,7 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
                 r.y = fminf(fmaxf(r.y, -30.0f), 30.0f) * kL2E;
                 r.z = fminf(fmaxf(r.z, -30.0f), 30.0f) * kL2E;
                 r.w = fminf(fmaxf(r.w, -30.0f), 30.0f) * kL2E;
-                reinterpret_cast<float4 *>(Rs)[v4] = r;
+                if (!TMIDX) reinterpret_cast<float4 *>(Rs)[v4] = r;      // TMIDX: R' goes to TMEM from L
                 reinterpret_cast<float4 *>(Ls)[v4] = r;
             }
         }
@@ -229,6 +233,26 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
 #pragma unroll
             for (int j = 0; j < WH0; ++j) e0[k][j] = 0.0f;
         __syncthreads();
+        if constexpr (TMIDX) {
+#pragma unroll
+            for (int k = 0; k < B0; ++k) {
+                const int r = pr0 + k * S0;
+                float rv[WR];
+                if (pr0 < S0 && r < mb) {
+                    lds_row<WR>(smem, lbase + uint32_t(r) * WR * 4u, rv);    // L = R' right after the ingest
+                } else {
+#pragma unroll
+                    for (int j = 0; j < WR; ++j) rv[j] = 0.0f;
+                }
+                asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(
+                                 tm_r0 + 8u * k),
+                             "r"(__float_as_uint(rv[0])), "r"(__float_as_uint(rv[1])), "r"(__float_as_uint(rv[2])),
+                             "r"(__float_as_uint(rv[3])), "r"(__float_as_uint(rv[4])), "r"(__float_as_uint(rv[5])),
+                             "r"(0u), "r"(0u)
+                             : "memory");
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
 
         int32_t iters = a.max_iter;
         bool stopped = false;
@@ -366,9 +390,21 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
                 const int r = pr0 + k * S0;
                 const bool act = pr0 < S0 && r < mb;
                 const unsigned pm = LPR0 > 1 ? __ballot_sync(0xffffffffu, act) : 0u;
+                uint32_t tr[TMIDX ? 8 : 1];
+                if constexpr (TMIDX) {
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                                 : "=r"(tr[0]), "=r"(tr[1]), "=r"(tr[2]), "=r"(tr[3]), "=r"(tr[4]), "=r"(tr[5]),
+                                   "=r"(tr[6]), "=r"(tr[7])
+                                 : "r"(tm_r0 + 8u * k)
+                                 : "memory");
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                }
                 if (act) {
                     float rv[WH0], lv[WH0];
-                    if (k < RP && !r_in_smem) {
+                    if constexpr (TMIDX) {
+#pragma unroll
+                        for (int j = 0; j < WH0; ++j) rv[j] = __uint_as_float(tr[j]);
+                    } else if (k < RP && !r_in_smem) {
 #pragma unroll
                         for (int j = 0; j < WH0; ++j) rv[j] = rpre[k < RP ? k : 0][j];
                     } else {
@@ -486,7 +522,7 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if ((tt >> 5) == 0)
-            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(s_tmem) : "memory");
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tmem) : "memory");
     }
 }
 
