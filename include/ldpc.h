@@ -190,9 +190,7 @@ ldpc_status ldpc_decode_workspace_bytes(const ldpc_code *code, int64_t frames,
  * early termination); 6 = 4 with 16-bit
  * offsets (n <= 16383); 7 exchange cluster kernel (same codes as 5; a
  * cluster of C CTAs per frame trades message segments with bulk DSMEM copies;
- * fixed iterations, wr = 6; its two-frames-in-flight form keeps the clamped,
- * rescaled R of each frame in flight in the workspace, C5: 7 clusters x 2 x
- * 259 KB); 8 lane-per-edge kernel (any H with
+ * fixed iterations, wr = 6; no workspace); 8 lane-per-edge kernel (any H with
  * row degree <= 32 whose E, L, R fit one SM's shared memory: a group of
  * 4/8/16/32 lanes per check row, one CTA per frame, no workspace; for batches
  * too small to fill the GPU with one thread per check row); 9 global-exchange

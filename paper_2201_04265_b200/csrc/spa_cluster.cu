@@ -447,6 +447,45 @@ __global__ void __launch_bounds__(MAXT, 1) xband_kernel(const XArgs a) {
     }
 }
 
+// Tensor Memory helpers (32x32b shapes: each lane of the warp its own TMEM lane)
+__device__ __forceinline__ void tm_ld4(uint32_t a, uint32_t (&v)[4]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                 : "r"(a)
+                 : "memory");
+}
+__device__ __forceinline__ void tm_ld2(uint32_t a, uint32_t &v0, uint32_t &v1) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(v0), "=r"(v1) : "r"(a) : "memory");
+}
+__device__ __forceinline__ void tm_ld8(uint32_t a, uint32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "r"(a)
+                 : "memory");
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_st4(uint32_t a, uint32_t v0, uint32_t v1, uint32_t v2, uint32_t v3) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v0), "r"(v1), "r"(v2),
+                 "r"(v3)
+                 : "memory");
+}
+__device__ __forceinline__ void tm_st2(uint32_t a, uint32_t v0, uint32_t v1) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(a), "r"(v0), "r"(v1) : "memory");
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// 6 words (WR = 6): x4 + x2
+__device__ __forceinline__ void tm_ld6(uint32_t a, uint32_t (&v)[6]) {
+    uint32_t t[4];
+    tm_ld4(a, t);
+    tm_ld2(a + 4, v[4], v[5]);
+    tm_wait_ld();
+    v[0] = t[0]; v[1] = t[1]; v[2] = t[2]; v[3] = t[3];
+}
+__device__ __forceinline__ void tm_st6(uint32_t a, const uint32_t (&v)[6]) {
+    tm_st4(a, v[0], v[1], v[2], v[3]);
+    tm_st2(a + 4, v[4], v[5]);
+}
+
 // ---------------------------------------------------------------------------
 // Two frames in flight per cluster (slots 0 and 1; H = 1, e.g. 16-CTA
 // clusters on C5).  Each slot has its own VAR / ROW regions and barriers; the
@@ -484,7 +523,11 @@ __global__ void __launch_bounds__(MAXT, 1) xband2_kernel(const XArgs a) {
     const int nkey = C * C * H * NC;
     const int32_t *varOff = code.xband_seg, *rowOff = code.xband_seg + nkey, *sbytes = code.xband_seg + 2 * nkey;
     auto key = [](int s, int d, int h, int c) { return ((s * C + d) * H + h) * NC + c; };
-    auto rslot = [&](int sl) { return a.rws + (size_t(cid) * 2 + size_t(sl)) * size_t(n); };
+    // R' (clamped, log2-scaled R) of the thread's band-0 row, per slot, in
+    // Tensor Memory (otherwise idle here): compute warp w owns lanes
+    // 32 (w % 4) .. + 31, columns 16 (w / 4) + 6 sl .. + 5; written at
+    // V-phase 0, read by every V-phase (it was an L2-resident slot)
+    __shared__ uint32_t s_tmem;
     {
         const uint32_t *src = reinterpret_cast<const uint32_t *>(code.xband_sidx + size_t(q) * nq * NB);
         for (int i = tt; i < nq * NB / 2; i += blockDim.x) {
@@ -500,6 +543,15 @@ __global__ void __launch_bounds__(MAXT, 1) xband2_kernel(const XArgs a) {
             }
         }
     }
+    const uint32_t warp = uint32_t(tt) >> 5;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(saddr(&s_tmem)) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tm_r = s_tmem + ((32u * (warp & 3u)) << 16) + 16u * (warp >> 2);
     uint32_t rx_l = 0, rx_e = 0;
     for (int s = 0; s < C; ++s)
         for (int c = 0; c < NC; ++c) {
@@ -589,24 +641,29 @@ __global__ void __launch_bounds__(MAXT, 1) xband2_kernel(const XArgs a) {
 #pragma unroll
             for (int sl = 0; sl < 2; ++sl) {
                 if (sl < ns) {
-                    float lv[WR];
+                    float lv[WR] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
                     if (own) {
                         const int v0 = (int(q) * mbq + r) * WR;
                         lds_row<WR>(reinterpret_cast<const char *>(a.llr + fs[sl] * int64_t(n)), uint32_t(v0) * 4u, lv);
 #pragma unroll
                         for (int j = 0; j < WR; ++j) lv[j] = fminf(fmaxf(lv[j], -30.0f), 30.0f) * kL2E;
-                        // R' of the slot's frame, reread by every V-phase (L2-resident workspace)
-                        sts_row<WR>(reinterpret_cast<char *>(rslot(sl)), uint32_t(v0) * 4u, lv);
                         const uint32_t *vt = vtab + size_t(r) * WR * NB;
 #pragma unroll
                         for (int j = 0; j < WR; ++j)
 #pragma unroll
                             for (int b = 0; b < NB; ++b) *reinterpret_cast<float *>(varr[sl] + vt[j * NB + b]) = lv[j];
                     }
+                    // R' of the slot's frame, reread by every V-phase (TMEM; all lanes)
+                    {
+                        const uint32_t u[6] = {__float_as_uint(lv[0]), __float_as_uint(lv[1]), __float_as_uint(lv[2]),
+                                               __float_as_uint(lv[3]), __float_as_uint(lv[4]), __float_as_uint(lv[5])};
+                        tm_st6(tm_r + 6u * uint32_t(sl), u);
+                    }
                     chunk_done(vchunk(sl));
                     if (own) check_row<WR, true>(lv, e0[sl]);
                 }
             }
+            tm_wait_st();
             for (int t = 1; t <= a.max_iter; ++t) {
                 // ---- C-phases (a3)
 #pragma unroll
@@ -639,8 +696,12 @@ __global__ void __launch_bounds__(MAXT, 1) xband2_kernel(const XArgs a) {
                 for (int sl = 0; sl < 2; ++sl) {
                     if (sl < ns) {
                         float lv[WR];
-                        if (own)
-                            lds_row<WR>(reinterpret_cast<const char *>(rslot(sl)), uint32_t((int(q) * mbq + r) * WR) * 4u, lv);
+                        {
+                            uint32_t u[6];
+                            tm_ld6(tm_r + 6u * uint32_t(sl), u);
+#pragma unroll
+                            for (int j = 0; j < WR; ++j) lv[j] = __uint_as_float(u[j]);
+                        }
                         wait_var(sl);
                         if (own) {
                             uint32_t s_[WR * NB];
@@ -740,6 +801,383 @@ __global__ void __launch_bounds__(MAXT, 1) xband2_kernel(const XArgs a) {
         }
         cluster_sync_all();
     }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(s_tmem) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// NS frames in flight per 16-CTA cluster with the per-thread constant state in
+// Tensor Memory (xbandt_kernel; C5 batches).  Same ownership, protocol,
+// arithmetic and adaptive votes as xband2_kernel; what moves:
+//   * the CTA's slot tables leave shared memory: compute thread r keeps its
+//     own rows -- the VAR slots of its band-0 row's WR x NB edges and the ROW
+//     slots of its band-b rows -- in TMEM columns of its warp (tcgen05.ld per
+//     phase, 12-cycle latency), which frees 32 KB of shared memory for a
+//     third slot (6 regions of ~33 KB);
+//   * the band-0 E of every slot also lives in TMEM (loaded for the slot's
+//     variable phase, stored after its band-0 check) instead of NS x WR
+//     registers, which spilled when a third slot was held in registers.
+// A third frame in flight gives every segment exchange two other slots'
+// phases of cover instead of one (the exchange is latency-, not
+// bandwidth-bound: DESIGN.md xband2_kernel).
+// TMEM layout (512 columns, one CTA per SM): compute warp w owns lanes
+// 32 (w % 4) .. + 31 and columns 64 (w / 4) .. + 63: [0, 12) VAR slots of the
+// band-0 row's edges (j NB + b), [12, 12 + WR NB) ROW slots of the band-b rows
+// (b WR + j), [24, 24 + WR NS) band-0 E of the slots.
+// Hard decisions go through a CTA byte array in shared memory (the words
+// that straddle two CTAs read the neighbour's through DSMEM).
+template <int WR, int WC, int C, int MAXT, int NFIX = 0, int NS = 3>
+__global__ void __launch_bounds__(MAXT, 1) xbandt_kernel(const XArgs a) {
+    static_assert(WR == 6 && WC == 3, "xbandt: the (3,6) layout of its TMEM columns");
+    extern __shared__ __align__(128) char smem[];
+    constexpr int NB = WC - 1, H = 1, NC = NB;
+    const DeviceCode &code = a.code;
+    const int n = NFIX ? NFIX : code.n, mb = NFIX ? NFIX / WR : code.mb, mbq = mb / C, nq = n / C;
+    const int TW = NFIX ? xband_threads(NFIX / WR / C) : int(blockDim.x) - 32, tt = threadIdx.x, lane = tt & 31;
+    const bool producer = tt >= TW;
+    const uint32_t cap_b = uint32_t(code.xcap) * 4u;
+    const uint32_t q = cluster_ctarank();
+    const int64_t cid = cluster_id_x(), ncl = ncluster_x();
+    // slot regions by offset (no per-slot pointer registers)
+    auto varr = [&](int sl) { return smem + 2u * uint32_t(sl) * cap_b; };
+    auto rowr = [&](int sl) { return smem + (2u * uint32_t(sl) + 1u) * cap_b; };
+    uint8_t *zscr = reinterpret_cast<uint8_t *>(smem + 2 * NS * cap_b);        // nq hard-decision bytes
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + ((2 * NS * cap_b + uint32_t(nq) + 15u) & ~15u));
+    constexpr int NBAR = 2 + H + NC;
+    int *flags = reinterpret_cast<int *>(bars + NS * NBAR);   // [NS][C]
+    __shared__ uint32_t s_tmem;
+    const uint32_t bar0 = saddr(bars);
+    auto vbar = [&](int sl) { return bar0 + 8u * uint32_t(sl * NBAR); };
+    auto rbar = [&](int sl) { return bar0 + 8u * uint32_t(sl * NBAR + 1); };
+    auto vchunk = [&](int sl) { return bar0 + 8u * uint32_t(sl * NBAR + 2); };
+    auto cchunk = [&](int sl, int c) { return bar0 + 8u * uint32_t(sl * NBAR + 3 + c); };
+    const int nkey = C * C * H * NC;
+    const int32_t *varOff = code.xband_seg, *rowOff = code.xband_seg + nkey, *sbytes = code.xband_seg + 2 * nkey;
+    auto key = [](int s, int d, int h, int c) { return ((s * C + d) * H + h) * NC + c; };
+    auto rslot = [&](int sl) { return a.rws + (size_t(cid) * NS + size_t(sl)) * size_t(n); };
+    const int r = tt;                 // H = 1: this thread's band-0 row (if r < mbq)
+    const bool own = !producer && r < mbq;
+
+    // ---- TMEM: allocate, then every compute thread parks its table rows
+    const uint32_t warp = uint32_t(tt) >> 5;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(saddr(&s_tmem)) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tm = s_tmem + ((32u * (warp & 3u)) << 16) + 64u * (warp >> 2);
+    const uint32_t tm_vt = tm, tm_rt = tm + 12, tm_e0 = tm + 24;
+    if (!producer) {
+        uint32_t v[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, w[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+        if (r < mbq) {
+            const uint32_t *src = reinterpret_cast<const uint32_t *>(code.xband_sidx + (size_t(q) * nq + size_t(r) * WR) * NB);
+#pragma unroll
+            for (int i = 0; i < WR * NB / 2; ++i) {
+                const uint32_t x = __ldg(src + i);
+                v[2 * i] = x & 0xffffu;
+                v[2 * i + 1] = x >> 16;
+            }
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                const uint32_t *rs =
+                    reinterpret_cast<const uint32_t *>(code.xband_ridx + size_t(b) * n + (size_t(q) * mbq + r) * WR);
+#pragma unroll
+                for (int i = 0; i < WR / 2; ++i) {
+                    const uint32_t x = __ldg(rs + i);
+                    w[b * WR + 2 * i] = x & 0xffffu;
+                    w[b * WR + 2 * i + 1] = x >> 16;
+                }
+            }
+        }
+        tm_st4(tm_vt, v[0], v[1], v[2], v[3]);
+        tm_st4(tm_vt + 4, v[4], v[5], v[6], v[7]);
+        tm_st4(tm_vt + 8, v[8], v[9], v[10], v[11]);
+        tm_st4(tm_rt, w[0], w[1], w[2], w[3]);
+        tm_st4(tm_rt + 4, w[4], w[5], w[6], w[7]);
+        tm_st4(tm_rt + 8, w[8], w[9], w[10], w[11]);
+        tm_wait_st();
+    }
+    uint32_t rx_l = 0, rx_e = 0;
+    for (int s = 0; s < C; ++s)
+        for (int c = 0; c < NC; ++c) {
+            rx_l += uint32_t(__ldg(sbytes + key(s, q, 0, c)));
+            rx_e += uint32_t(__ldg(sbytes + key(q, s, 0, c)));
+        }
+    if (tt == 0) {
+        for (int sl = 0; sl < NS; ++sl) {
+            mbar_init(vbar(sl), 1);
+            mbar_init(rbar(sl), 1);
+            mbar_init(vchunk(sl), uint32_t(TW / 32));
+            for (int c = 0; c < NC; ++c) mbar_init(cchunk(sl, c), uint32_t(TW / 32));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int sl = 0; sl < NS; ++sl) {
+            mbar_arm(vbar(sl), rx_e);
+            mbar_arm(rbar(sl), rx_l);
+        }
+    }
+    cluster_sync_all();
+
+    auto chunk_done = [&](uint32_t bar) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_local(bar);
+    };
+    // barrier phase parities, one bit per slot
+    uint32_t nv = 0, nc = 0, nl = 0, ne = 0;
+    auto ship_l = [&](int sl) {
+        mbar_wait(vchunk(sl), (nv >> sl) & 1u);
+        const uint32_t vs = saddr(varr(sl)), rs = saddr(rowr(sl));
+        for (int i = lane; i < C * NC; i += 32) {
+            const int d = i / NC, c = i - d * NC;
+            const int k = key(int(q), d, 0, c);
+            const uint32_t nbytes = uint32_t(__ldg(sbytes + k));
+            if (nbytes)
+                bulk_s2c(mapa_u32(rs + uint32_t(__ldg(rowOff + k)), uint32_t(d)), vs + uint32_t(__ldg(varOff + k)), nbytes,
+                         mapa_u32(rbar(sl), uint32_t(d)));
+        }
+        nv ^= 1u << sl;
+    };
+    auto ship_e = [&](int sl, int c) {
+        mbar_wait(cchunk(sl, c), (nc >> sl) & 1u);
+        const uint32_t vs = saddr(varr(sl)), rs = saddr(rowr(sl));
+        if (lane < C) {
+            const int s = lane;
+            const int k = key(s, int(q), 0, c);
+            const uint32_t nbytes = uint32_t(__ldg(sbytes + k));
+            if (nbytes)
+                bulk_s2c(mapa_u32(vs + uint32_t(__ldg(varOff + k)), uint32_t(s)), rs + uint32_t(__ldg(rowOff + k)), nbytes,
+                         mapa_u32(vbar(sl), uint32_t(s)));
+        }
+        if (c == NC - 1) nc ^= 1u << sl;
+    };
+    auto wait_row = [&](int sl) {
+        mbar_wait(rbar(sl), (nl >> sl) & 1u);
+        if (tt == 0) mbar_arm(rbar(sl), rx_l);
+        nl ^= 1u << sl;
+    };
+    auto wait_var = [&](int sl) {
+        mbar_wait(vbar(sl), (ne >> sl) & 1u);
+        if (tt == 0) mbar_arm(vbar(sl), rx_e);
+        ne ^= 1u << sl;
+    };
+    auto e0_store = [&](int sl, const float (&e)[WR]) {
+        const uint32_t u[6] = {__float_as_uint(e[0]), __float_as_uint(e[1]), __float_as_uint(e[2]),
+                               __float_as_uint(e[3]), __float_as_uint(e[4]), __float_as_uint(e[5])};
+        tm_st6(tm_e0 + uint32_t(WR * sl), u);
+    };
+
+    const int64_t ngroups = (a.frames + NS - 1) / NS;
+    for (int64_t pi = cid; pi < ngroups; pi += ncl) {
+        auto fs = [&](int sl) { return int64_t(NS) * pi + sl; };
+        // per-slot bits: syndrome of the slot's frame, votes on, a vote hit
+        uint32_t synd = 0, vote_on = (1u << NS) - 1u, hit = 0;
+        const int ns = int(std::min<int64_t>(NS, a.frames - int64_t(NS) * pi));    // cluster-uniform
+        if (producer) {
+            for (int sl = 0; sl < ns; ++sl) ship_l(sl);
+            for (int t = 1; t <= a.max_iter; ++t) {
+                for (int sl = 0; sl < ns; ++sl)
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) ship_e(sl, c);
+                for (int sl = 0; sl < ns; ++sl) ship_l(sl);
+            }
+        } else {
+            // ---- V-phase 0 of every slot: L = R, E = 0; band-0 check of t = 1
+#pragma unroll
+            for (int sl = 0; sl < NS; ++sl) {
+                if (sl < ns) {
+                    uint32_t vt[12];
+                    tm_ld8(tm_vt, *reinterpret_cast<uint32_t(*)[8]>(vt));
+                    tm_ld4(tm_vt + 8, *reinterpret_cast<uint32_t(*)[4]>(vt + 8));
+                    tm_wait_ld();
+                    float lv[WR], e0n[WR];
+                    if (own) {
+                        const int v0 = (int(q) * mbq + r) * WR;
+                        lds_row<WR>(reinterpret_cast<const char *>(a.llr + fs(sl) * int64_t(n)), uint32_t(v0) * 4u, lv);
+#pragma unroll
+                        for (int j = 0; j < WR; ++j) lv[j] = fminf(fmaxf(lv[j], -30.0f), 30.0f) * kL2E;
+                        sts_row<WR>(reinterpret_cast<char *>(rslot(sl)), uint32_t(v0) * 4u, lv);
+#pragma unroll
+                        for (int j = 0; j < WR; ++j)
+#pragma unroll
+                            for (int b = 0; b < NB; ++b) *reinterpret_cast<float *>(varr(sl) + vt[j * NB + b]) = lv[j];
+                    }
+                    chunk_done(vchunk(sl));
+                    if (own) check_row<WR, true>(lv, e0n);
+                    e0_store(sl, e0n);
+                }
+            }
+            tm_wait_st();
+            for (int t = 1; t <= a.max_iter; ++t) {
+                // ---- C-phases (a3)
+#pragma unroll
+                for (int sl = 0; sl < NS; ++sl) {
+                    if (sl < ns) {
+                        if (a.adapt_votes) {
+                            const bool on = ((hit >> sl) & 1u) || (t & 3) == 1;
+                            vote_on = (vote_on & ~(1u << sl)) | (uint32_t(on) << sl);
+                            hit &= ~(1u << sl);
+                        }
+                        wait_row(sl);
+#pragma unroll
+                        for (int b = 0; b < NB; ++b) {
+                            uint32_t s_[WR];
+                            tm_ld6(tm_rt + uint32_t(b * WR), s_);
+                            if (r < mbq) {
+                                float x[WR], e[WR];
+#pragma unroll
+                                for (int j = 0; j < WR; ++j) x[j] = *reinterpret_cast<const float *>(rowr(sl) + s_[j]);
+                                hit |= uint32_t(check_row_gated<WR>(x, e, (vote_on >> sl) & 1u)) << sl;
+#pragma unroll
+                                for (int j = 0; j < WR; ++j) *reinterpret_cast<float *>(rowr(sl) + s_[j]) = e[j];
+                            }
+                            chunk_done(cchunk(sl, b));
+                        }
+                    }
+                }
+                // ---- V-phases (a4/a5)
+                const bool last = t == a.max_iter;
+#pragma unroll
+                for (int sl = 0; sl < NS; ++sl) {
+                    if (sl < ns) {
+                        float lv[WR], e0c[WR];
+                        if (own)
+                            lds_row<WR>(reinterpret_cast<const char *>(rslot(sl)), uint32_t((int(q) * mbq + r) * WR) * 4u, lv);
+                        uint32_t s_[WR * NB];
+                        {
+                            uint32_t eu[6];
+                            tm_ld8(tm_vt, *reinterpret_cast<uint32_t(*)[8]>(s_));
+                            tm_ld4(tm_vt + 8, *reinterpret_cast<uint32_t(*)[4]>(s_ + 8));
+                            tm_ld4(tm_e0 + uint32_t(WR * sl), *reinterpret_cast<uint32_t(*)[4]>(eu));
+                            tm_ld2(tm_e0 + uint32_t(WR * sl) + 4, eu[4], eu[5]);
+                            tm_wait_ld();
+#pragma unroll
+                            for (int j = 0; j < WR; ++j) e0c[j] = __uint_as_float(eu[j]);
+                        }
+                        wait_var(sl);
+                        if (own) {
+                            float eb[WR * NB];
+#pragma unroll
+                            for (int j = 0; j < WR; ++j) {
+                                lv[j] += e0c[j];
+#pragma unroll
+                                for (int b = 0; b < NB; ++b) {
+                                    eb[j * NB + b] = *reinterpret_cast<const float *>(varr(sl) + s_[j * NB + b]);
+                                    lv[j] += eb[j * NB + b];
+                                }
+                            }
+                            if (last) {
+                                uint32_t rp = 0;
+#pragma unroll
+                                for (int j = 0; j < WR; ++j) {
+                                    rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
+#pragma unroll
+                                    for (int b = 0; b < NB; ++b) *reinterpret_cast<float *>(varr(sl) + s_[j * NB + b]) = lv[j];
+                                }
+                                synd |= (rp & 1u) << sl;
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < WR; ++j) {
+#pragma unroll
+                                    for (int b = 0; b < NB; ++b)
+                                        *reinterpret_cast<float *>(varr(sl) + s_[j * NB + b]) = lv[j] - eb[j * NB + b];
+                                    lv[j] -= e0c[j];
+                                }
+                            }
+                        }
+                        chunk_done(vchunk(sl));
+                        if (!last) {
+                            if (own) hit |= uint32_t(check_row_gated<WR>(lv, e0c, (vote_on >> sl) & 1u)) << sl;
+                            e0_store(sl, e0c);
+                        }
+                    }
+                }
+                tm_wait_st();
+            }
+            // ---- a7: syndrome of the CTA's rows (ROW slots hold L of bands >= 1)
+#pragma unroll
+            for (int sl = 0; sl < NS; ++sl) {
+                if (sl < ns) {
+                    wait_row(sl);
+#pragma unroll
+                    for (int b = 0; b < NB; ++b) {
+                        uint32_t s_[WR];
+                        tm_ld6(tm_rt + uint32_t(b * WR), s_);
+                        if (r < mbq) {
+                            uint32_t rp = 0;
+#pragma unroll
+                            for (int j = 0; j < WR; ++j) rp ^= (*reinterpret_cast<const float *>(rowr(sl) + s_[j]) >= 0.0f) ? 1u : 0u;
+                            synd |= (rp & 1u) << sl;
+                        }
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int sl = 0; sl < NS; ++sl) {
+            const int any = __syncthreads_or(((synd >> sl) & 1u) != 0);
+            if (tt == 0) {
+                int *f0 = cg::this_cluster().map_shared_rank(flags, 0);
+                f0[sl * C + int(q)] = any;
+            }
+        }
+        cluster_sync_all();
+        // ---- a6/a8, slot by slot: L_v sits in the VAR slot of (v, band 1);
+        // each thread writes its own row's posteriors and hard-decision bytes,
+        // then whole words are packed (the word straddling into the next CTA
+        // reads its bytes through DSMEM)
+        const int nw = code.nw;
+        const int w_lo = (int(q) * nq + 31) / 32;
+        const int w_hi = (int(q) == C - 1) ? nw : ((int(q) + 1) * nq + 31) / 32;
+        const int qn = (int(q) + 1 < C) ? int(q) + 1 : int(q);
+        const uint8_t *znext = cg::this_cluster().map_shared_rank(zscr, qn);
+        for (int sl = 0; sl < ns; ++sl) {
+            if (!producer) {
+                uint32_t vt[12];
+                tm_ld8(tm_vt, *reinterpret_cast<uint32_t(*)[8]>(vt));
+                tm_ld4(tm_vt + 8, *reinterpret_cast<uint32_t(*)[4]>(vt + 8));
+                tm_wait_ld();
+                if (own) {
+#pragma unroll
+                    for (int j = 0; j < WR; ++j) {
+                        const float lv = *reinterpret_cast<const float *>(varr(sl) + vt[j * NB]);
+                        zscr[r * WR + j] = lv >= 0.0f ? 1 : 0;
+                        if (a.posterior) a.posterior[fs(sl) * int64_t(n) + int64_t(q) * nq + r * WR + j] = lv * kLn2;
+                    }
+                }
+            }
+            cluster_sync_all();             // every CTA's bytes are written
+            if (!producer) {
+                uint32_t *bits = a.bits + fs(sl) * int64_t(nw);
+                for (int base = w_lo * 32; base < w_hi * 32; base += TW) {
+                    const int v = base + tt;
+                    if (v >= w_hi * 32) break;
+                    bool z = false;
+                    if (v < n) {
+                        const int i = v - int(q) * nq;
+                        z = (i < nq ? zscr[i] : znext[i - nq]) != 0;
+                    }
+                    const uint32_t word = __ballot_sync(0xffffffffu, z);
+                    if (lane == 0) bits[v >> 5] = word;
+                }
+                if (q == 0 && tt == 0) {
+                    int ok = 1;
+                    for (int i = 0; i < C; ++i) ok &= (flags[sl * C + i] == 0);
+                    a.syn_ok[fs(sl)] = uint8_t(ok);
+                    a.iters[fs(sl)] = a.max_iter;
+                }
+            }
+            cluster_sync_all();             // the byte arrays are reused by the next slot / frame
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tmem) : "memory");
 }
 
 template <int WR, int H, int MAXT>
@@ -786,6 +1224,33 @@ bool xcluster_plan(const ldpc_code &c, int64_t frames, bool et, XClusterPlan &p)
     p.threads = ((mbq + H - 1) / H + 31) / 32 * 32 + 32;     // compute warps + the producer warp
     // two frames in flight per cluster (xband2_kernel) when the view allows it
     // and the batch has at least two frames per co-resident cluster's worth
+    // three frames in flight with the per-thread tables and band-0 E in TMEM
+    // (xbandt_kernel): 6 regions + the hard-decision bytes in shared memory.
+    // Opt-in (LDPC_XTMEM=1): measured 0.321 of the SFU model against 0.360 for
+    // xband2_kernel
+    if (c.dev.xslots == 2 && H == 1 && frames >= 3 && c.wr == 6 && c.wc == 3 && p.threads <= 768 && C == 16 &&
+        !std::getenv("LDPC_XBAND_1SLOT") && std::getenv("LDPC_XTMEM") && std::atoi(std::getenv("LDPC_XTMEM")) == 1) {
+        constexpr int NS = 3;
+        const size_t nq = size_t(c.n / C);
+        const size_t smem3 = 2 * NS * size_t(c.dev.xcap) * 4 + nq + 16 + 16 + size_t(NS) * 8 * (3 + size_t(c.wc - 1)) +
+                             size_t(NS) * 4 * size_t(C);
+        void *k3 = (c.n == 64800 && !std::getenv("LDPC_NO_NFIX"))
+                       ? reinterpret_cast<void *>(&xbandt_kernel<6, 3, 16, 768, 64800, NS>)
+                       : reinterpret_cast<void *>(&xbandt_kernel<6, 3, 16, 768, 0, NS>);
+        if (smem3 + 1024 <= 227 * 1024 && ensure_smem_attribute(k3, smem3, true)) {
+            int ncl = occupancy_clusters(k3, p.threads, smem3, C);
+            if (ncl >= 1) {
+                p.kernel = k3;
+                p.cluster = C;
+                p.smem = smem3;
+                p.capacity = NS * int64_t(ncl);
+                ncl = int(std::min<int64_t>(ncl, (frames + NS - 1) / NS));
+                p.grid = ncl * C;
+                p.ws_bytes = size_t(ncl) * NS * size_t(c.n) * 4;     // R' per (cluster, slot)
+                return true;
+            }
+        }
+    }
     if (c.dev.xslots == 2 && H == 1 && frames >= 2 && c.wr == 6 && c.wc == 3 && p.threads <= 768 &&
         !std::getenv("LDPC_XBAND_1SLOT")) {
         void *k2 = nullptr;
@@ -803,7 +1268,7 @@ bool xcluster_plan(const ldpc_code &c, int64_t frames, bool et, XClusterPlan &p)
                     p.capacity = 2 * int64_t(ncl);
                     ncl = int(std::min<int64_t>(ncl, (frames + 1) / 2));
                     p.grid = ncl * C;
-                    p.ws_bytes = size_t(ncl) * 2 * size_t(c.n) * 4;     // R' per (cluster, slot)
+                    p.ws_bytes = 0;     // R' lives in TMEM
                     return true;
                 }
             }
