@@ -311,9 +311,11 @@ __device__ __forceinline__ bool check_row(const float (&x)[D], float (&e)[D], co
 #pragma unroll
         for (int j = 1; j < D; ++j) lo = fminf(lo, ax[j]);
         if (__all_sync(__activemask(), lo >= sat_bound<D>())) {
+            // sign(e_j) = sign(sx) ^ sign(x_j), magnitude E_MAX: with t =
+            // sign(sx) | E_MAX once per row, one 3-input LOP3 per element
+            const uint32_t tsat = (sx & 0x80000000u) | __float_as_uint(kEMaxB);
 #pragma unroll
-            for (int j = 0; j < D; ++j)
-                e[j] = __uint_as_float(__float_as_uint(kEMaxB) | ((sx ^ __float_as_uint(x[j])) & 0x80000000u));
+            for (int j = 0; j < D; ++j) e[j] = __uint_as_float((__float_as_uint(x[j]) & 0x80000000u) ^ tsat);
             return true;
         }
     }
@@ -322,9 +324,10 @@ __device__ __forceinline__ bool check_row(const float (&x)[D], float (&e)[D], co
 #pragma unroll
         for (int j = 1; j < D; ++j) lo = fminf(lo, ax[j]);
         if (cm && __all_sync(__activemask(), lo >= kClampB)) {
+            const uint32_t sxm = sx & 0x80000000u;
 #pragma unroll
             for (int j = 0; j < D; ++j)
-                e[j] = __uint_as_float(__float_as_uint(cm[j]) | ((sx ^ __float_as_uint(x[j])) & 0x80000000u));
+                e[j] = __uint_as_float(__float_as_uint(cm[j]) | ((__float_as_uint(x[j]) & 0x80000000u) ^ sxm));
             return true;
         }
     }
@@ -379,9 +382,9 @@ __device__ __forceinline__ void check_row_pair(const float (&x)[D / 2], float (&
 #pragma unroll
         for (int j = 1; j < W; ++j) lo = fminf(lo, ax[j]);
         if (__all_sync(__activemask(), lo >= sat_bound<D>())) {
+            const uint32_t tsat = (sx & 0x80000000u) | __float_as_uint(kEMaxB);
 #pragma unroll
-            for (int j = 0; j < W; ++j)
-                e[j] = __uint_as_float(__float_as_uint(kEMaxB) | ((sx ^ __float_as_uint(x[j])) & 0x80000000u));
+            for (int j = 0; j < W; ++j) e[j] = __uint_as_float((__float_as_uint(x[j]) & 0x80000000u) ^ tsat);
             return;
         }
     }
@@ -453,6 +456,58 @@ __device__ __forceinline__ void check_any(const float (&x)[D / LPR], float (&e)[
         check_row_pair<D, VOTE>(x, e, h, pm);
     }
 }
+
+// Tensor Memory as per-thread storage (32x32b shapes: lane i of the warp
+// reads / writes TMEM lane (lane base + i); N consecutive columns).
+template <int N>
+__device__ __forceinline__ void tmem_st(uint32_t a, const uint32_t (&v)[N]) {
+    static_assert(N == 2 || N == 4 || N == 8 || N == 16, "tcgen05.st shapes used here");
+    if constexpr (N == 2) {
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(a), "r"(v[0]), "r"(v[1]) : "memory");
+    } else if constexpr (N == 4) {
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v[0]), "r"(v[1]),
+                     "r"(v[2]), "r"(v[3])
+                     : "memory");
+    } else if constexpr (N == 8) {
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(a), "r"(v[0]),
+                     "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                     : "memory");
+    } else {
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+            "%15, %16};" ::"r"(a),
+            "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+            "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+            : "memory");
+    }
+}
+template <int N>
+__device__ __forceinline__ void tmem_ld(uint32_t a, uint32_t (&v)[N]) {
+    static_assert(N == 2 || N == 4 || N == 8 || N == 16, "tcgen05.ld shapes used here");
+    if constexpr (N == 2) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "r"(a) : "memory");
+    } else if constexpr (N == 4) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                     : "r"(a)
+                     : "memory");
+    } else if constexpr (N == 8) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                     : "r"(a)
+                     : "memory");
+    } else {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+            "%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+              "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(a)
+            : "memory");
+    }
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+constexpr int pow2_at_least(int x) { return x <= 2 ? 2 : x <= 4 ? 4 : x <= 8 ? 8 : x <= 16 ? 16 : x <= 32 ? 32 : x <= 64 ? 64 : x <= 128 ? 128 : x <= 256 ? 256 : 512; }
 
 template <int D>
 __device__ __forceinline__ void lds_row(const char *smem, uint32_t byte_off, float (&o)[D]) {

@@ -160,44 +160,50 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
 
     unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};       // GEN: this CTA's counters (thread 0)
     __shared__ int s_err[2];
-    // TMIDX (C4: n = 16200, 16-bit offsets, one lane per row): the packed L
-    // offsets of this thread's B1 rows of bands >= 1 are constant for the
-    // whole launch.  They live in Tensor Memory (256 columns, otherwise idle
-    // here) instead of being re-read through L1/L2 every iteration: warp w
-    // owns lanes 32 (w % 4) .. + 31 and columns 4 B1 (w / 4) ..; row k's three
-    // words sit at column 4 k of that range (tcgen05.ld, 12-cycle latency).
-    constexpr bool TMIDX = L16 && LPR == 1 && NFIX == 16200 && !GEN && WR == 6 && BAND_TMEM_OFFSETS;
-    // ... and columns 256 + 8 B0 (w / 4) ..: the R' of this thread's band-0
-    // rows (row k at + 8 k), copied from L = R' at each frame's ingest and
-    // read by every variable phase (it lived in an L2-resident slot)
+    // TMIDX (compile-time n with 16-bit offsets and one lane per row: C4):
+    // constant per-thread data lives in Tensor Memory (otherwise idle
+    // here) instead of being re-read every iteration -- the packed L offsets
+    // of the thread's B1 rows of bands >= 1 (from L1/L2; written once per
+    // launch) and the R' of its B0 band-0 rows (from an L2 slot, C4, or
+    // shared memory, C3; copied from L = R' at each frame's ingest).  Warp w
+    // owns lanes 32 (w % 4) .. + 31 and PERW columns from PERW (w / 4): row
+    // k's offsets at OFFW k, its R' at B1 OFFW + RW k (tcgen05.ld, 12-cycle
+    // latency).  The CTA allocates TMCOLS (a power of two; C3 runs 2-3 CTAs
+    // per SM, all fit the 512 columns).
+    // (C3 at 2-3 CTAs per SM with R in shared memory measured much worse with
+    // it: 1.20 -> 0.95, 1.13 -> 1.00, 0.79 -> 0.59 of the SFU model -- C4 only.)
+    constexpr bool TMIDX = L16 && LPR == 1 && LPR0 == 1 && !GEN && NFIX == 16200 && BAND_TMEM_OFFSETS;
+    constexpr int OFFW = pow2_at_least(WR / 2), RW = pow2_at_least(WR);
+    constexpr int PERW = B1 * OFFW + B0 * RW;
+    constexpr int TMCOLS = TMIDX ? pow2_at_least(PERW * ((TFIX / 32 + 3) / 4) < 32 ? 32 : PERW * ((TFIX / 32 + 3) / 4)) : 32;
+    static_assert(!TMIDX || TMCOLS <= 256 || NFIX == 16200, "TMEM columns of a multi-CTA kernel");
     __shared__ uint32_t s_tmem;
     uint32_t tm_row0 = 0, tm_r0 = 0;
     if constexpr (TMIDX) {
-        static_assert(4 * B1 * ((TFIX / 32 + 3) / 4) <= 256 && 8 * B0 * ((TFIX / 32 + 3) / 4) <= 256, "TMEM columns");
         const uint32_t warp = uint32_t(tt) >> 5;
         if (warp == 0) {
             const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&s_tmem));
-            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(dst) : "memory");
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(dst), "n"(TMCOLS)
+                         : "memory");
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        tm_row0 = s_tmem + ((32u * (warp & 3u)) << 16) + 4u * uint32_t(B1) * (warp >> 2);
-        tm_r0 = s_tmem + ((32u * (warp & 3u)) << 16) + 256u + 8u * uint32_t(B0) * (warp >> 2);
+        tm_row0 = s_tmem + ((32u * (warp & 3u)) << 16) + uint32_t(PERW) * (warp >> 2);
+        tm_r0 = tm_row0 + uint32_t(B1 * OFFW);
 #pragma unroll
         for (int k = 0; k < B1; ++k) {
             const int r = pr + k * S;
-            uint32_t w0 = 0, w1 = 0, w2 = 0;
+            uint32_t w[OFFW];
+#pragma unroll
+            for (int i = 0; i < OFFW; ++i) w[i] = 0u;
             if (pr < S && r < NB * mb) {
                 const uint32_t *p16 = reinterpret_cast<const uint32_t *>(code.band_lidx16 + size_t(r) * WR);
-                w0 = __ldg(p16);
-                w1 = __ldg(p16 + 1);
-                w2 = __ldg(p16 + 2);
+#pragma unroll
+                for (int i = 0; i < WR / 2; ++i) w[i] = __ldg(p16 + i);
             }
-            asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(tm_row0 + 4u * k), "r"(w0),
-                         "r"(w1), "r"(w2), "r"(0u)
-                         : "memory");
+            tmem_st<OFFW>(tm_row0 + uint32_t(OFFW * k), w);
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
@@ -250,18 +256,15 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
             for (int k = 0; k < B0; ++k) {
                 const int r = pr0 + k * S0;
                 float rv[WR];
+                uint32_t u[RW];
+#pragma unroll
+                for (int j = 0; j < RW; ++j) u[j] = 0u;
                 if (pr0 < S0 && r < mb) {
                     lds_row<WR>(smem, lbase + uint32_t(r) * WR * 4u, rv);    // L = R' right after the ingest
-                } else {
 #pragma unroll
-                    for (int j = 0; j < WR; ++j) rv[j] = 0.0f;
+                    for (int j = 0; j < WR; ++j) u[j] = __float_as_uint(rv[j]);
                 }
-                asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(
-                                 tm_r0 + 8u * k),
-                             "r"(__float_as_uint(rv[0])), "r"(__float_as_uint(rv[1])), "r"(__float_as_uint(rv[2])),
-                             "r"(__float_as_uint(rv[3])), "r"(__float_as_uint(rv[4])), "r"(__float_as_uint(rv[5])),
-                             "r"(0u), "r"(0u)
-                             : "memory");
+                tmem_st<RW>(tm_r0 + uint32_t(RW * k), u);
             }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
@@ -323,14 +326,8 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
                 const int r = pr + k * S;
                 const bool act = pr < S && r < NB * mb;
                 const unsigned pm = LPR > 1 ? __ballot_sync(0xffffffffu, act) : 0u;
-                uint32_t tmw[TMIDX ? 4 : 1];
-                if constexpr (TMIDX) {
-                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
-                                 : "=r"(tmw[0]), "=r"(tmw[1]), "=r"(tmw[2]), "=r"(tmw[3])
-                                 : "r"(tm_row0 + 4u * k)
-                                 : "memory");
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                }
+                uint32_t tmw[TMIDX ? OFFW : 1];
+                if constexpr (TMIDX) tmem_ld<OFFW>(tm_row0 + uint32_t(OFFW * k), tmw);
                 if (act) {
                     int32_t li[WH];
                     float e[WH], x[WH];
@@ -412,15 +409,8 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
                 const int r = pr0 + k * S0;
                 const bool act = pr0 < S0 && r < mb;
                 const unsigned pm = LPR0 > 1 ? __ballot_sync(0xffffffffu, act) : 0u;
-                uint32_t tr[TMIDX ? 8 : 1];
-                if constexpr (TMIDX) {
-                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                                 : "=r"(tr[0]), "=r"(tr[1]), "=r"(tr[2]), "=r"(tr[3]), "=r"(tr[4]), "=r"(tr[5]),
-                                   "=r"(tr[6]), "=r"(tr[7])
-                                 : "r"(tm_r0 + 8u * k)
-                                 : "memory");
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                }
+                uint32_t tr[TMIDX ? RW : 1];
+                if constexpr (TMIDX) tmem_ld<RW>(tm_r0 + uint32_t(RW * k), tr);
                 if (act) {
                     float rv[WH0], lv[WH0];
                     if constexpr (TMIDX) {
@@ -545,7 +535,7 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if ((tt >> 5) == 0)
-            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_tmem) : "memory");
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "n"(TMCOLS) : "memory");
     }
 }
 
