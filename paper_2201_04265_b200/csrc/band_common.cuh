@@ -297,20 +297,22 @@ __host__ __device__ constexpr bool has_clamp_tier() { return sat_bound<D>() > kC
 // has_clamp_tier<D>() and VOTE; may be null otherwise).
 template <int D, bool VOTE>
 __device__ __forceinline__ bool check_row(const float (&x)[D], float (&e)[D], const float *cm = nullptr) {
-    float f[D], ax[D];
+    float f[D];
     uint32_t sx = (D & 1) ? 0x80000000u : 0u;     // (-1)^{d_c}
 #pragma unroll
-    for (int j = 0; j < D; ++j) {
-        sx ^= __float_as_uint(x[j]);
-        ax[j] = fminf(fabsf(x[j]), kClampB);
+    for (int j = 0; j < D; ++j) sx ^= __float_as_uint(x[j]);
+    // min_j |x_j| decides both shortcut tiers before the clamped inputs are
+    // formed (both bounds are <= the clamp, so min |x| >= b <=> min
+    // min(|x|, clamp) >= b: the same decisions)
+    float lo_abs = fabsf(x[0]);
+    if constexpr (VOTE && (sat_bound<D>() <= kClampB || has_clamp_tier<D>())) {
+#pragma unroll
+        for (int j = 1; j < D; ++j) lo_abs = fminf(lo_abs, fabsf(x[j]));
     }
     if constexpr (VOTE && sat_bound<D>() <= kClampB) {
         // saturated rows (every input at the clamp: a converged frame under
         // fixed iterations): E = +-E_MAX exactly as the full update gives it
-        float lo = ax[0];
-#pragma unroll
-        for (int j = 1; j < D; ++j) lo = fminf(lo, ax[j]);
-        if (__all_sync(__activemask(), lo >= sat_bound<D>())) {
+        if (__all_sync(__activemask(), lo_abs >= sat_bound<D>())) {
             // sign(e_j) = sign(sx) ^ sign(x_j), magnitude E_MAX: with t =
             // sign(sx) | E_MAX once per row, one 3-input LOP3 per element
             const uint32_t tsat = (sx & 0x80000000u) | __float_as_uint(kEMaxB);
@@ -320,10 +322,7 @@ __device__ __forceinline__ bool check_row(const float (&x)[D], float (&e)[D], co
         }
     }
     if constexpr (VOTE && has_clamp_tier<D>()) {
-        float lo = ax[0];
-#pragma unroll
-        for (int j = 1; j < D; ++j) lo = fminf(lo, ax[j]);
-        if (cm && __all_sync(__activemask(), lo >= kClampB)) {
+        if (cm && __all_sync(__activemask(), lo_abs >= kClampB)) {
             const uint32_t sxm = sx & 0x80000000u;
 #pragma unroll
             for (int j = 0; j < D; ++j)
@@ -331,6 +330,9 @@ __device__ __forceinline__ bool check_row(const float (&x)[D], float (&e)[D], co
             return true;
         }
     }
+    float ax[D];
+#pragma unroll
+    for (int j = 0; j < D; ++j) ax[j] = fminf(fabsf(x[j]), kClampB);
     bool hit = psi_row<D, true, VOTE>(ax, f);
     float ex[D];
     exclusive_sums<D>(f, ex);
