@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_psi.py -q -m gpu -x -k "c3 or c4 or explicit or simulate or saturation or check_row or c5_sampled" > gpurun_out/lop2_tests.log 2>&1; echo EXIT $? >> gpurun_out/lop2_tests.log
+bash tools/ab_quick.sh lop2 "C3-R1/4:100000 C3-R1/2:100000 C3-R3/4:100000 C4:200000 C5:16384" "lop2||paper_2201_04265_b200/libldpc_b200.so"
