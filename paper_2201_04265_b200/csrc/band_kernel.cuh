@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
     // per SM, all fit the 512 columns).
     // (C3 at 2-3 CTAs per SM with R in shared memory measured much worse with
     // it: 1.20 -> 0.95, 1.13 -> 1.00, 0.79 -> 0.59 of the SFU model -- C4 only.)
-    constexpr bool TMIDX = L16 && LPR == 1 && LPR0 == 1 && !GEN && NFIX == 16200 && BAND_TMEM_OFFSETS;
+    constexpr bool TMIDX = L16 && LPR == 1 && LPR0 == 1 && NFIX == 16200 && BAND_TMEM_OFFSETS;
     constexpr int OFFW = pow2_at_least(WR / 2), RW = pow2_at_least(WR);
     constexpr int PERW = B1 * OFFW + B0 * RW;
     constexpr int TMCOLS = TMIDX ? pow2_at_least(PERW * ((TFIX / 32 + 3) / 4) < 32 ? 32 : PERW * ((TFIX / 32 + 3) / 4)) : 32;
