@@ -69,6 +69,9 @@ __device__ __forceinline__ bool cta_sync_or(bool p) { return __syncthreads_or(p 
 #ifndef BAND_LPR2_MINB
 #define BAND_LPR2_MINB 5
 #endif
+#ifndef BAND_C3R34_MINB
+#define BAND_C3R34_MINB 3      // C3 R3/4 (352 threads): 3 blocks per SM, 56 registers (2 blocks, 80 registers, no spill: 0.795 vs 0.805)
+#endif
 #ifndef BAND_T1R34_MINB
 #define BAND_T1R34_MINB 8      // Table I R3/4 (96 threads): 80 registers, no spill
 #endif
@@ -84,7 +87,7 @@ __device__ __forceinline__ bool cta_sync_or(bool p) { return __syncthreads_or(p 
 constexpr int band_lb_minb(int wr, int nfix, int lpr, int wc = 0) {
     return lpr == 2 ? BAND_LPR2_MINB
          : !BAND_NFIX_MINB ? 1
-         : nfix == 1008 ? 7 : nfix == 3996 ? (wr == 12 ? 3 : wr == 4 ? 3 : 2)
+         : nfix == 1008 ? 7 : nfix == 3996 ? (wr == 12 ? BAND_C3R34_MINB : wr == 4 ? 3 : 2)
          : (nfix == 1032 && wc == 3) ? BAND_T1R34_MINB : 1;
 }
 constexpr int band_lb_threads(int wr, int wc, int b0, int nfix, int lpr) {
