@@ -11,6 +11,9 @@
 #ifndef BAND_ADAPT_VOTES
 #define BAND_ADAPT_VOTES 1
 #endif
+#ifndef BAND_C1_INTERLEAVE
+#define BAND_C1_INTERLEAVE 1
+#endif
 #ifndef BAND_TMEM_OFFSETS
 #define BAND_TMEM_OFFSETS 1
 #endif
@@ -103,7 +106,14 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
     band_kernel(const BandArgs a) {
     // measured on B200: +1.1 points on C4 (MODE 2), +0.8..1.3 on wr = 12 codes,
     // -2..3 on check-major wr = 4 / 6 codes (C3 R1/4, R1/2)
-    constexpr bool FUSE0 = BAND_FUSE0 && (MODE == 2 || WR >= 12 || NOVOTE);
+    // C1I (C1: n = 96, band-0 rows on lane pairs, no votes, fixed
+    // iterations): every lane has one band-0 half row and one row of bands
+    // 1-2.  The check phase runs both updates in one block so their two
+    // dependency chains interleave (a 1000-frame C1 batch is one latency-bound
+    // wave); the band-0 check therefore leaves the variable phase (no FUSE0).
+    constexpr bool C1I = BAND_C1_INTERLEAVE && NFIX == 96 && LPR == 1 && LPR0 == 2 && B0 == 1 && !ET && NOVOTE &&
+                         MODE == 0 && !GEN;
+    constexpr bool FUSE0 = BAND_FUSE0 && (MODE == 2 || WR >= 12 || NOVOTE) && !C1I;
     // Adaptive psi votes (one lane per row): a warp votes in iteration t only
     // if one of its votes hit in t - 1, or t = 1 mod 4.  Votes that keep
     // failing (rows straddling the regime split) cost ~5 instructions per
@@ -304,8 +314,23 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
             }
             // ---- a3: check-node phase (and syndrome of z^{t-1} when ET)
             uint32_t synd = FUSE0 ? synd0 : 0u;
+            if constexpr (C1I) {
+                const int r0 = pr0, r = pr;          // every lane: r0 < mb, r < NB mb
+                float lv0[WH0], x0[WH0], x[WR], e[WR];
+                lds_row<WH0>(smem, lbase + (uint32_t(r0) * WR + hoff0) * 4u, lv0);
 #pragma unroll
-            for (int k = 0; k < (FUSE0 ? 0 : B0); ++k) {
+                for (int j = 0; j < WH0; ++j) x0[j] = lv0[j] - e0[0][j];
+                int32_t li[WR];
+                ldg_idx<WR>(lidx + size_t(r) * WR, li);
+                lds_row<WR>(smem, uint32_t(r) * WR * 4u, e);
+#pragma unroll
+                for (int j = 0; j < WR; ++j) x[j] = *reinterpret_cast<const float *>(smem + li[j]) - e[j];
+                check_row_pair<WR, false>(x0, e0[0], h0, 0xffffffffu);
+                check_row<WR, false>(x, e);
+                sts_row<WR>(smem, uint32_t(r) * WR * 4u, e);
+            }
+#pragma unroll
+            for (int k = 0; k < (FUSE0 || C1I ? 0 : B0); ++k) {
                 const int r = pr0 + k * S0;
                 const bool act = pr0 < S0 && r < mb;
                 const unsigned pm = LPR0 > 1 ? __ballot_sync(0xffffffffu, act) : 0u;
@@ -325,7 +350,7 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
                 }
             }
 #pragma unroll
-            for (int k = 0; k < B1; ++k) {
+            for (int k = 0; k < (C1I ? 0 : B1); ++k) {
                 const int r = pr + k * S;
                 const bool act = pr < S && r < NB * mb;
                 const unsigned pm = LPR > 1 ? __ballot_sync(0xffffffffu, act) : 0u;
