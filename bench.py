@@ -45,7 +45,8 @@ E2E_PINNED_BYTES = 16e9          # pinned host memory for the e2e arm, over all 
 KERNEL_NAMES = {1: "spa_decode_kernel (generic, on-chip)", 2: "spa_decode_kernel (generic, global state)",
                 3: "band_kernel (check-major E)", 4: "band_kernel (variable-major E)",
                 5: "band_cluster_kernel (L2 gathers)", 6: "band_kernel (variable-major E, 16-bit offsets)",
-                7: "xband_kernel (exchange cluster, bulk DSMEM segments)",
+                7: "xband_kernel (exchange cluster, bulk DSMEM segments; C5 batches: two-frame 16-CTA clusters "
+                   "plus gband2_kernel groups on the SMs the clusters leave idle)",
                 8: "edge_kernel (lane per edge, small batches)",
                 9: "gband2_kernel (16-CTA groups, segments through L2 staging)"}
 

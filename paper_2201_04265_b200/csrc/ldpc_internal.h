@@ -300,6 +300,8 @@ struct XClusterPlan {
     int64_t capacity = 0;       // frames decoded concurrently (co-resident clusters)
     size_t smem = 0;
     size_t ws_bytes = 0;
+    int slots = 1;              // frames in flight per cluster
+    int64_t pairs_capacity() const { return slots == 2 ? capacity / 2 : 0; }
 };
 // Launch plan of the global-exchange kernel (spa_gexchange.cu; variant 9):
 // groups of 16 co-resident CTAs (cooperative launch) on the 16-CTA exchange
@@ -315,10 +317,14 @@ struct GXPlan {
     size_t zero_bytes = 0;      // workspace prefix zeroed per launch (arrival / barrier counters)
     size_t off_arrivals = 0, off_gbar = 0, off_stage = 0, off_rws = 0, off_zbyte = 0, off_synd = 0;
 };
-bool gx_plan(const ldpc_code &c, int64_t frames, bool et, GXPlan &p);
+// max_groups > 0 caps the groups (the tail on the SMs exchange clusters leave
+// idle); dependent = launched as the programmatic dependent of the kernel
+// before it on the stream (no cooperative attribute, no memset: the caller
+// zeroes zero_bytes before the primary launch)
+bool gx_plan(const ldpc_code &c, int64_t frames, bool et, GXPlan &p, int max_groups = 0);
 ldpc_status gx_launch(const ldpc_code &c, const GXPlan &p, const float *llr, int64_t frames, const ldpc_decode_opts &o,
                       uint32_t *bits, uint8_t *syn, int32_t *iters, float *post, void *ws, size_t ws_bytes,
-                      void *stream);
+                      void *stream, bool dependent = false);
 
 // false unless the bound code has an exchange cluster view, fixed iterations
 // and an instantiated (wc, wr, rows-per-thread, C).

@@ -506,6 +506,10 @@ __global__ void __launch_bounds__(MAXT, 1) xband2_kernel(const XArgs a) {
     const uint32_t cap_b = uint32_t(code.xcap) * 4u;
     const uint32_t q = cluster_ctarank();
     const int64_t cid = cluster_id_x(), ncl = ncluster_x();
+    // every CTA of this grid is resident (one wave of clusters): let a
+    // dependent launch (the global-exchange tail on the SMs 16-CTA clusters
+    // leave idle, xcluster_launch) start now instead of after this grid
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     char *varr[2] = {smem, smem + 2 * cap_b};
     char *rowr[2] = {smem + cap_b, smem + 3 * cap_b};
     // slot tables widened to 32-bit byte offsets in shared memory (vector
@@ -1244,6 +1248,7 @@ bool xcluster_plan(const ldpc_code &c, int64_t frames, bool et, XClusterPlan &p)
                 p.cluster = C;
                 p.smem = smem3;
                 p.capacity = NS * int64_t(ncl);
+                p.slots = NS;
                 ncl = int(std::min<int64_t>(ncl, (frames + NS - 1) / NS));
                 p.grid = ncl * C;
                 p.ws_bytes = size_t(ncl) * NS * size_t(c.n) * 4;     // R' per (cluster, slot)
@@ -1266,6 +1271,7 @@ bool xcluster_plan(const ldpc_code &c, int64_t frames, bool et, XClusterPlan &p)
                     p.cluster = C;
                     p.smem = smem2;
                     p.capacity = 2 * int64_t(ncl);
+                    p.slots = 2;
                     ncl = int(std::min<int64_t>(ncl, (frames + 1) / 2));
                     p.grid = ncl * C;
                     p.ws_bytes = 0;     // R' lives in TMEM

@@ -482,7 +482,42 @@ struct Resolved {
     GXPlan gx;
     ClusterPlan cl;
     Plan gen;
+    // variant 7 with two-frame 16-CTA clusters: the last tail_frames frames run
+    // on the global-exchange kernel over the SMs those clusters leave idle,
+    // launched as their programmatic dependent (tail_plan)
+    GXPlan tail;
+    int64_t tail_frames = 0;
 };
+
+// Frames for the global-exchange tail next to xband2_kernel's clusters: 16-CTA
+// clusters place 7 per B200 (112 SMs), so 36 SMs hold two more 16-CTA groups.
+// The split balances the two kernels' rounds of frame pairs: a group decodes a
+// pair at `rate` x a cluster's speed (LDPC_XTAIL_RATE; measured on C5 beside
+// the clusters: 0.326 ms per cluster round, 0.59 ms per group round, i.e.
+// 0.55).  The default sits a little below the balance point: a tail
+// that finishes early idles 32 SMs briefly, one that finishes late holds up
+// the whole batch.  LDPC_XTAIL=0 turns the tail off.  Only for batches of many
+// rounds, where the split's rounding is small.
+void tail_plan(const ldpc_code &c, int64_t frames, const ldpc_decode_opts &o, Resolved &r) {
+    r.tail_frames = 0;
+    const char *env = std::getenv("LDPC_XTAIL");
+    if (env && std::atoi(env) == 0) return;
+    if (r.x.cluster != 16 || r.x.pairs_capacity() < 1) return;
+    const int64_t sms = device_attribute(cudaDevAttrMultiProcessorCount);
+    const int idle = int(sms - r.x.pairs_capacity() * r.x.cluster);
+    const int groups = idle / 16;
+    if (groups < 1) return;
+    const double rate = std::getenv("LDPC_XTAIL_RATE") ? std::atof(std::getenv("LDPC_XTAIL_RATE")) : 0.53;
+    const int64_t pairs = (frames + 1) / 2;
+    const double share = groups * rate / (groups * rate + double(r.x.pairs_capacity()));
+    const int64_t min_rounds = 8;
+    if (pairs < min_rounds * (r.x.pairs_capacity() + groups)) return;
+    int64_t tail_pairs = int64_t(double(pairs) * share / groups + 0.5) * groups;
+    if (tail_pairs < groups) return;
+    if (!gx_plan(c, 2 * tail_pairs, o.early_term != 0, r.tail, groups)) return;
+    r.tail_frames = std::min<int64_t>(2 * tail_pairs, frames - 2);
+}
+
 ldpc_status resolve(const ldpc_code &c, int64_t frames, const ldpc_decode_opts &o, Resolved &r) {
     const int v = o.variant;
     const bool et = o.early_term != 0;
@@ -520,6 +555,7 @@ ldpc_status resolve(const ldpc_code &c, int64_t frames, const ldpc_decode_opts &
     if (v == 7) {
         if (!x_ok) return LDPC_ERR_UNSUPPORTED;
         r.variant = 7;
+        tail_plan(c, frames, o, r);
         return LDPC_OK;
     }
     if (v == 9) {
@@ -558,6 +594,7 @@ ldpc_status resolve(const ldpc_code &c, int64_t frames, const ldpc_decode_opts &
             return LDPC_OK;
         }
         r.variant = 7;
+        tail_plan(c, frames, o, r);
         return LDPC_OK;
     }
     if (v == 0 || v == 5) {
@@ -599,7 +636,7 @@ ldpc_status ldpc_decode_workspace_bytes(const ldpc_code *code, int64_t frames, c
     if (s != LDPC_OK) return s;
     switch (r.variant) {
         case 3: case 4: case 6: *bytes = r.band.ws_bytes; break;
-        case 7: *bytes = r.x.ws_bytes; break;
+        case 7: *bytes = r.tail_frames ? std::max(r.x.ws_bytes, r.tail.ws_bytes) : r.x.ws_bytes; break;
         case 9: *bytes = r.gx.ws_bytes; break;
         case 5: *bytes = r.cl.ws_bytes; break;
         // variant 8 needs none; where the band kernel could decode the code, its
@@ -626,9 +663,25 @@ ldpc_status ldpc_decode(const ldpc_code *code, const float *d_llr, int64_t frame
         case 3: case 4: case 6:
             return ldpc::band_launch(*code, r.band, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters, d_posterior,
                                      d_ws, ws_bytes, stream);
-        case 7:
-            return ldpc::xcluster_launch(*code, r.x, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters,
-                                         d_posterior, d_ws, ws_bytes, stream);
+        case 7: {
+            if (!r.tail_frames)
+                return ldpc::xcluster_launch(*code, r.x, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters,
+                                             d_posterior, d_ws, ws_bytes, stream);
+            // frames [0, f1) on the exchange clusters, [f1, frames) on the
+            // global-exchange groups beside them (tail_plan); the tail's
+            // counters are zeroed first so nothing separates the two launches
+            if (r.x.ws_bytes || !d_ws || ws_bytes < r.tail.ws_bytes) return LDPC_ERR_ARG;
+            const int64_t f1 = frames - r.tail_frames;
+            if (cudaMemsetAsync(d_ws, 0, r.tail.zero_bytes, static_cast<cudaStream_t>(stream)) != cudaSuccess)
+                return LDPC_ERR_CUDA;
+            const ldpc_status s1 = ldpc::xcluster_launch(*code, r.x, d_llr, f1, *opts, d_bits, d_syndrome_ok, d_iters,
+                                                         d_posterior, nullptr, 0, stream);
+            if (s1 != LDPC_OK) return s1;
+            const int64_t nw = code->dev.nw, n = code->dev.n;
+            return ldpc::gx_launch(*code, r.tail, d_llr + f1 * n, r.tail_frames, *opts, d_bits + f1 * nw,
+                                   d_syndrome_ok + f1, d_iters + f1, d_posterior ? d_posterior + f1 * n : nullptr,
+                                   d_ws, ws_bytes, stream, true);
+        }
         case 9:
             return ldpc::gx_launch(*code, r.gx, d_llr, frames, *opts, d_bits, d_syndrome_ok, d_iters, d_posterior,
                                    d_ws, ws_bytes, stream);

@@ -437,11 +437,16 @@ __global__ void __launch_bounds__(MAXT, 1) gband2_kernel(const GXArgs a) {
             }
         }
     }
+    // launched as the dependent of xband2_kernel (the tail on the SMs its
+    // clusters leave idle): this grid completes only after that one has, so
+    // whatever the stream runs next sees both grids' outputs (a no-op for a
+    // plain launch)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 }  // namespace
 
-bool gx_plan(const ldpc_code &c, int64_t frames, bool et, GXPlan &p) {
+bool gx_plan(const ldpc_code &c, int64_t frames, bool et, GXPlan &p, int max_groups_cap) {
     if (et || !c.gallager || !c.regular_col || !c.dev.xcluster || c.dev.xslots != 2 || c.wr != 6 || c.wc != 3)
         return false;
     constexpr int G = 16;
@@ -461,7 +466,8 @@ bool gx_plan(const ldpc_code &c, int64_t frames, bool et, GXPlan &p) {
         return false;
     }
     const int sms = device_attribute(cudaDevAttrMultiProcessorCount);
-    const int max_groups = sms * per_sm / G;
+    int max_groups = sms * per_sm / G;
+    if (max_groups_cap > 0) max_groups = std::min(max_groups, max_groups_cap);
     if (max_groups < 1) return false;
     p.groups = int(std::min<int64_t>(max_groups, std::max<int64_t>(1, (frames + 1) / 2)));
     p.kernel = k;
@@ -482,11 +488,11 @@ bool gx_plan(const ldpc_code &c, int64_t frames, bool et, GXPlan &p) {
 
 ldpc_status gx_launch(const ldpc_code &c, const GXPlan &p, const float *llr, int64_t frames, const ldpc_decode_opts &o,
                       uint32_t *bits, uint8_t *syn, int32_t *iters, float *post, void *ws, size_t ws_bytes,
-                      void *stream) {
+                      void *stream, bool dependent) {
     if (!ws || ws_bytes < p.ws_bytes) return LDPC_ERR_ARG;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     char *w = static_cast<char *>(ws);
-    if (cudaMemsetAsync(w, 0, p.zero_bytes, s) != cudaSuccess) return LDPC_ERR_CUDA;
+    if (!dependent && cudaMemsetAsync(w, 0, p.zero_bytes, s) != cudaSuccess) return LDPC_ERR_CUDA;
     GXArgs a;
     a.code = c.dev;
     a.llr = llr;
@@ -506,8 +512,18 @@ ldpc_status gx_launch(const ldpc_code &c, const GXPlan &p, const float *llr, int
     a.synd = reinterpret_cast<int32_t *>(w + p.off_synd);
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
+    if (dependent) {
+        // starts once every CTA of the exchange-cluster grid before it is
+        // resident (griddepcontrol.launch_dependents there), on the SMs those
+        // clusters leave free; no cooperative attribute: the 16 CTAs of a group
+        // are co-resident because the grid fits the idle SMs, and a CTA that
+        // had to wait for the primary grid to drain only delays its group
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+    } else {
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+    }
     cfg.gridDim = dim3(unsigned(p.grid));
     cfg.blockDim = dim3(unsigned(p.threads));
     cfg.dynamicSmemBytes = p.smem;
