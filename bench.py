@@ -654,13 +654,31 @@ def measure_point(args, L, code, wl, point, dev, rank, world, launched, sms, pro
 
 
 def encode_roofline(work, count, enc_ms, sms, clock_mhz):
-    """Encode (e1, Eq. 3): the parity bits are M.P over GF(2), one
-    LOP3 (acc ^= m & p) per 32 bit-MACs: (n - k) ceil(k/32) LOP3 per frame,
-    on the INT/ALU pipe; peak = the LOP3 rate measured by
-    tools/microbench_lop.cu (profiles/peaks_extra.json)."""
+    """Encode (e1, Eq. 3): the parity bits are M.P over GF(2).
+    Long messages in large batches run it on the tensor cores
+    (encode_mma.cu: 0/1 bytes, exact int32 dot products, parity = LSB):
+    2 k (n - k) int8 ops per frame against the int8 dense peak, taken as the
+    measured bf16 peak (MEASURED_PEAKS.json) x the nominal int8/bf16 ratio 2.
+    Otherwise the INT-pipe kernel: one LOP3 (acc ^= m & p) per 32 bit-MACs,
+    (n - k) ceil(k/32) LOP3 per frame against the LOP3 rate measured by
+    tools/microbench_lop.cu (profiles/peaks_extra.json).  The time is the
+    whole ldpc_encode call (parity product + assemble into H order)."""
     if enc_ms <= 0 or count == 0:
         return None
     kw = (work.k + 31) // 32
+    chunk = min((m for _, m in work.spans if m > 0), default=0)
+    if kw >= 16 and chunk >= 512 and os.environ.get("LDPC_ENC_MMA", "") != "0":
+        pk = measured_peaks()
+        bf16 = float(pk.get("bf16_tflops", 0.0) or 0.0)
+        basis = (f"2 x measured bf16 {bf16:.1f} TFLOP/s (MEASURED_PEAKS.json, burst; nominal int8/bf16 ratio 2)"
+                 if bf16 > 0 else "nominal 4500 TOPS int8 dense (B200_PROFILING.md fallback)")
+        peak = 2.0 * bf16 if bf16 > 0 else 4500.0
+        ops = float(count) * 2.0 * work.k * (work.n - work.k)
+        ach = ops / (enc_ms / 1e3) / 1e12
+        return {"bound": "tensor", "kernel": "encode_mma_kernel (tcgen05.mma kind::i8, TMEM accumulators) + "
+                                               "encode_assemble_warp_kernel (ldpc_encode)",
+                "achieved": ach, "peak": peak, "unit": "T int8-op/s", "frac": ach / peak, "ms_per_step": enc_ms,
+                "algorithmic_ops_per_frame": 2 * work.k * (work.n - work.k), "peak_basis": basis}
     ops = float(count) * (work.n - work.k) * kw
     per_clk, basis = 64.0, "assumed 64 LOP3/clk/SM (ALU pipe, 16 lanes/clk/SMSP)"
     try:

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "channel_common.cuh"
 #include "ldpc_internal.h"
@@ -131,6 +132,45 @@ __global__ void __launch_bounds__(256) encode_assemble_kernel(const DeviceCode c
             if ((threadIdx.x & 31) == 0) row[v >> 5] = word;
         }
         __syncthreads();
+    }
+}
+
+// Assemble, warp per frame (n <= 65536): the inverse permutation lives in
+// shared memory as 16-bit positions, loaded once per CTA, and every warp
+// scatters whole frames with its own staging rows -- no CTA barrier per
+// frame, and pinv is not re-read from L2 for every frame (it was 4 bytes per
+// codeword bit and frame in encode_assemble_kernel).  Same output bits.
+constexpr int kAsmWarps = 8;
+__global__ void __launch_bounds__(kAsmWarps * 32) encode_assemble_warp_kernel(const DeviceCode code,
+                                                                              const uint32_t *__restrict__ info,
+                                                                              uint32_t *__restrict__ cw,
+                                                                              int64_t frames) {
+    extern __shared__ __align__(16) uint32_t asm_smem[];
+    const int kw = code.kw, nw = code.nw, k = code.k, n = code.n;
+    const int npw = (n - k + 31) / 32;
+    const int rw = kw + npw;
+    uint16_t *pinv16 = reinterpret_cast<uint16_t *>(asm_smem + size_t(kAsmWarps) * rw);
+    for (int v = threadIdx.x; v < n; v += blockDim.x) pinv16[v] = uint16_t(__ldg(code.pinv + v));
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t *mrow = asm_smem + size_t(warp) * rw, *prow = mrow + kw;
+    const int64_t gw = int64_t(blockIdx.x) * kAsmWarps + warp, nwarps = int64_t(gridDim.x) * kAsmWarps;
+    for (int64_t f = gw; f < frames; f += nwarps) {
+        uint32_t *row = cw + f * int64_t(nw);
+        for (int i = lane; i < kw; i += 32) mrow[i] = __ldg(info + f * int64_t(kw) + i);
+        for (int i = lane; i < npw; i += 32) prow[i] = row[nw - npw + i];
+        __syncwarp();
+        for (int v0 = 0; v0 < nw * 32; v0 += 32) {
+            const int v = v0 + lane;
+            uint32_t bit = 0u;
+            if (v < n) {
+                const int t = pinv16[v];
+                bit = t < k ? (mrow[t >> 5] >> (t & 31)) & 1u : (prow[(t - k) >> 5] >> ((t - k) & 31)) & 1u;
+            }
+            const uint32_t word = __ballot_sync(0xffffffffu, bit != 0u);
+            if (lane == 0) row[v0 >> 5] = word;
+        }
+        __syncwarp();
     }
 }
 
@@ -302,12 +342,39 @@ ldpc_status ldpc_encode(const ldpc_code *code, const uint32_t *d_info, uint32_t 
         ldpc::encode_small_kernel<<<dim3(unsigned(std::max(grid, 1))), 256, 0, s>>>(D, d_info, d_cw, frames);
         return cudaGetLastError() == cudaSuccess ? LDPC_OK : LDPC_ERR_CUDA;
     }
-    const unsigned col_tiles = unsigned(D.npar_pad / ldpc::kEncColTile);
+    // parity words: on the tensor cores (encode_mma.cu) for long messages in
+    // large batches, else the INT-pipe binary GEMM; identical bits
+    cudaError_t merr = cudaSuccess;
+    const bool mma = ldpc::encode_parity_mma(D, d_info, d_cw, frames, s, &merr);
+    if (merr != cudaSuccess) return LDPC_ERR_CUDA;
+    const unsigned col_tiles = mma ? 0u : unsigned(D.npar_pad / ldpc::kEncColTile);
     const int64_t max_chunk = int64_t(65535) * ldpc::kEncTF;      // gridDim.y limit
     for (int64_t f0 = 0; f0 < frames && col_tiles > 0; f0 += max_chunk) {
         const int64_t nf = std::min<int64_t>(max_chunk, frames - f0);
         const dim3 grid(col_tiles, unsigned((nf + ldpc::kEncTF - 1) / ldpc::kEncTF));
         ldpc::encode_parity_kernel<<<grid, 256, 0, s>>>(D, d_info + f0 * D.kw, d_cw + f0 * D.nw, nf);
+    }
+    const size_t smemw = sizeof(uint32_t) * size_t(ldpc::kAsmWarps) * size_t(D.kw + (D.n - D.k + 31) / 32) +
+                         sizeof(uint16_t) * size_t(D.n);
+    const char *aenv = std::getenv("LDPC_ASM_WARP");
+    // only where >= 2 CTAs (16 warps) fit an SM: C5's 194 KB per CTA leaves 8
+    // warps per SM, measured slower than the CTA-per-frame kernel (74.7 vs
+    // 66.0 ms per 65,536 frames; C4 15.1 -> 14.1 ms per 200,000)
+    if (D.n <= 65536 && smemw <= 108 * 1024 && !(aenv && std::atoi(aenv) == 0)) {
+        static size_t attr = 0;
+        if (smemw > 48 * 1024 && smemw > attr) {
+            if (cudaFuncSetAttribute(ldpc::encode_assemble_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(smemw)) != cudaSuccess)
+                return LDPC_ERR_CUDA;
+            attr = smemw;
+        }
+        // as many CTAs per SM as shared memory holds (C4: 4, i.e. 32 warps)
+        const int per_sm = int(std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / (smemw + 1024))));
+        const int grid = int(std::min<int64_t>((frames + ldpc::kAsmWarps - 1) / ldpc::kAsmWarps,
+                                               int64_t(ldpc::sm_count()) * per_sm));
+        ldpc::encode_assemble_warp_kernel<<<std::max(grid, 1), ldpc::kAsmWarps * 32, smemw, s>>>(D, d_info, d_cw,
+                                                                                              frames);
+        return cudaGetLastError() == cudaSuccess ? LDPC_OK : LDPC_ERR_CUDA;
     }
     const size_t smem = sizeof(uint32_t) * size_t(D.kw + (D.n - D.k + 31) / 32);
     if (smem > 48 * 1024 &&

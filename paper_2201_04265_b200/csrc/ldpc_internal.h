@@ -326,6 +326,11 @@ ldpc_status gx_launch(const ldpc_code &c, const GXPlan &p, const float *llr, int
                       uint32_t *bits, uint8_t *syn, int32_t *iters, float *post, void *ws, size_t ws_bytes,
                       void *stream, bool dependent = false);
 
+// The encoder's parity words on the tensor cores (encode_mma.cu); false when
+// the code or batch stays on the INT-pipe kernel (LDPC_ENC_MMA=0/1 forces).
+bool encode_parity_mma(const DeviceCode &D, const uint32_t *d_info, uint32_t *d_cw, int64_t frames,
+                       cudaStream_t s, cudaError_t *err);
+
 // false unless the bound code has an exchange cluster view, fixed iterations
 // and an instantiated (wc, wr, rows-per-thread, C).
 bool xcluster_plan(const ldpc_code &c, int64_t frames, bool et, XClusterPlan &p);
