@@ -667,7 +667,9 @@ def encode_roofline(work, count, enc_ms, sms, clock_mhz):
         return None
     kw = (work.k + 31) // 32
     chunk = min((m for _, m in work.spans if m > 0), default=0)
-    if kw >= 16 and chunk >= 512 and os.environ.get("LDPC_ENC_MMA", "") != "0":
+    npp = (work.n - work.k + 127) // 128 * 128
+    tiles = (chunk + 255) // 256 * ((npp + 255) // 256)      # encode_mma.cu's rule: tiles >= SMs
+    if kw >= 16 and tiles >= sms and os.environ.get("LDPC_ENC_MMA", "") != "0":
         pk = measured_peaks()
         bf16 = float(pk.get("bf16_tflops", 0.0) or 0.0)
         basis = (f"2 x measured bf16 {bf16:.1f} TFLOP/s (MEASURED_PEAKS.json, burst; nominal int8/bf16 ratio 2)"

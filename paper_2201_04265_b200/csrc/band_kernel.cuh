@@ -17,6 +17,9 @@
 #ifndef BAND_TMEM_OFFSETS
 #define BAND_TMEM_OFFSETS 1
 #endif
+#ifndef BAND_EDET
+#define BAND_EDET 1
+#endif
 
 struct BandArgs {
     DeviceCode code;
@@ -124,6 +127,13 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
     // the wr = 12 codes use it, and early termination stays vote-free.
     constexpr bool ADAPT = BAND_ADAPT_VOTES && !NOVOTE && !ET && LPR == 1 && LPR0 == 1 && (NFIX == 16200 || WR >= 12);
     constexpr bool VM = MODE >= 1, L16 = MODE == 2;
+    // EDET: early termination decided at the end of the variable phase
+    // (BAND_EDET, measured: DESIGN.md "C2")
+    constexpr bool EDET = ET && BAND_EDET;
+    // CSYN: the check phase carries the syndrome of z^{t-1} and the stop test
+    // (ET without EDET; with EDET that test could never fire: the variable
+    // phase of t - 1 has already tested the same z)
+    constexpr bool CSYN = ET && !EDET;
     static_assert(LPR == 1 || (LPR == 2 && NFIX && !GEN && RPRE == 0 && WR % 2 == 0), "lane pairs: NFIX kernels");
     constexpr int WH = WR / LPR;          // elements of a row per lane
     extern __shared__ __align__(16) char smem[];
@@ -341,9 +351,9 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
 #pragma unroll
                     for (int j = 0; j < WH0; ++j) {
                         x[j] = lv[j] - e0[k][j];
-                        if (ET) rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
+                        if (CSYN) rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
                     }
-                    if (ET && LPR0 > 1) rp ^= __shfl_xor_sync(pm, rp, 1);
+                    if (CSYN && LPR0 > 1) rp ^= __shfl_xor_sync(pm, rp, 1);
                     synd |= rp;
                     if constexpr (ADAPT) vhit |= check_row_gated<WR>(x, e0[k], vote_on, cmp);
                     else check_any<WR, !ET && !NOVOTE, LPR0>(x, e0[k], h0, pm, cmp);
@@ -394,9 +404,9 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
                     for (int j = 0; j < WH; ++j) {
                         const float lv = *reinterpret_cast<const float *>(smem + li[j]);
                         x[j] = lv - e[j];
-                        if (ET) rp ^= (lv >= 0.0f) ? 1u : 0u;
+                        if (CSYN) rp ^= (lv >= 0.0f) ? 1u : 0u;
                     }
-                    if (ET && LPR > 1) rp ^= __shfl_xor_sync(pm, rp, 1);
+                    if (CSYN && LPR > 1) rp ^= __shfl_xor_sync(pm, rp, 1);
                     synd |= rp;
                     if constexpr (ADAPT) vhit |= check_row_gated<WR>(x, e, vote_on, cmp);
                     else check_any<WR, !ET && !NOVOTE, LPR>(x, e, h, pm, cmp);
@@ -420,7 +430,7 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
                     if (pr < S && r < mb) lds_row<WR>(reinterpret_cast<const char *>(Rs), uint32_t(r) * WR * 4u, rpre[k]);
                 }
             }
-            if (ET) {
+            if (CSYN) {
                 const bool any = cta_sync_or(synd != 0);
                 if (t > 1 && !any) {      // z^{t-1} has zero syndrome: stop (reading c6)
                     iters = t - 1;
@@ -432,6 +442,7 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
             }
             // ---- a4/a5: variable-node phase, Eq. 7 (owners of band-0 rows)
             synd0 = 0;
+            uint32_t sv0 = 0;           // EDET: band-0 rows' syndrome bits of z^t
 #pragma unroll
             for (int k = 0; k < B0; ++k) {
                 const int r = pr0 + k * S0;
@@ -473,8 +484,15 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
                         }
                     }
                     sts_row<WH0>(smem, lbase + (uint32_t(r) * WR + hoff0) * 4u, lv);
+                    if constexpr (EDET) {
+                        uint32_t rp = 0;
+#pragma unroll
+                        for (int j = 0; j < WH0; ++j) rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
+                        if (LPR0 > 1) rp ^= __shfl_xor_sync(pm, rp, 1);
+                        sv0 |= rp;
+                    }
                     if constexpr (FUSE0) {
-                        if (ET) {
+                        if (CSYN) {
                             uint32_t rp = 0;      // this band-0 row's syndrome bit of z^t (Eq. 1)
 #pragma unroll
                             for (int j = 0; j < WH0; ++j) rp ^= (lv[j] >= 0.0f) ? 1u : 0u;
@@ -491,7 +509,32 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
                     }
                 }
             }
-            __syncthreads();
+            if constexpr (EDET) {
+                // early detection (reading c6 / Q11): when no band-0 row of
+                // z^t is unsatisfied, test the other bands' rows at once (sign
+                // gathers only) and stop here -- iters = t, the posteriors just
+                // written -- instead of one check phase later, whose psi work
+                // would be thrown away.  Same stopping iteration and outputs.
+                if (t < a.max_iter && !cta_sync_or(sv0 != 0)) {
+                    uint32_t s12 = 0;
+                    for (int r = tt; r < NB * mb; r += T) {
+                        uint32_t rp = 0;
+#pragma unroll
+                        for (int j = 0; j < WR; ++j)
+                            rp ^= (*reinterpret_cast<const float *>(smem + __ldg(lidx + size_t(r) * WR + j)) >= 0.0f)
+                                      ? 1u
+                                      : 0u;
+                        s12 |= rp;
+                    }
+                    if (!cta_sync_or(s12 != 0)) {
+                        iters = t;
+                        stopped = true;
+                        break;
+                    }
+                }
+            } else {
+                __syncthreads();
+            }
         }
         // ---- a7: final syndrome when the loop ran to max_iter
         bool ok = stopped;

@@ -236,8 +236,11 @@ bool encode_parity_mma(const DeviceCode &D, const uint32_t *d_info, uint32_t *d_
     const char *env = std::getenv("LDPC_ENC_MMA");
     if (env && std::atoi(env) == 0) return false;
     const bool force = env && std::atoi(env) == 1;
-    // the INT-pipe kernel is as fast on short messages and small batches
-    if (!force && (D.kw < 16 || frames < 512)) return false;
+    // the INT-pipe kernel is as fast on short messages, and faster where the
+    // 256 x 256 tiles would not fill the GPU (Table I at 1000 frames: 8 tiles,
+    // measured 3.38 -> 3.23 Gbit/s on the MMA path)
+    const int64_t tiles = (frames + kMmaTileM - 1) / kMmaTileM * ((D.npar_pad + kMmaTileN - 1) / kMmaTileN);
+    if (!force && (D.kw < 16 || tiles < int64_t(device_attribute(cudaDevAttrMultiProcessorCount)))) return false;
     static bool attr_ok = false;
     if (!attr_ok) {
         if (cudaFuncSetAttribute(encode_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMmaSmem)) !=
