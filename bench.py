@@ -852,7 +852,22 @@ def e2e_measure(L, code, wl, args, dev, frame0, count, k, world):
     if F <= 0:
         return {"value": None, "unit": "Gbit/s", "error": "no frames on this rank"}
     Fc = min(F, args.e2e_chunk)              # pipeline chunk
-    nchunks = (F + Fc - 1) // Fc
+    # chunk sizes ramp up from Fc/8 by x2.5: the pipeline's fill (the first
+    # chunk's H2D, which nothing overlaps) shrinks 8x, and each next chunk's
+    # H2D still lands before the compute of the one before it ends (H2D of a
+    # frame is faster than its decode)
+    # (multiples of the SM count, so each chunk's decode ends in full waves)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    if F > Fc and Fc >= 8 * sms:
+        Fc = Fc // sms * sms
+    sizes, a = [], 0
+    c = max(1, Fc // 8 // sms * sms if Fc >= 8 * sms else Fc // 8) if F > Fc else F
+    while a < F:
+        m = min(c, F - a)
+        sizes.append((a, m))
+        a += m
+        c = min(Fc, int(c * 2.5) // sms * sms if c >= sms else int(c * 2.5))
+    nchunks = len(sizes)
     try:
         h_info = torch.empty((F, kw), dtype=torch.int32, pin_memory=True)
         h_llr = torch.empty((F, n), dtype=torch.float32, pin_memory=True)
@@ -869,7 +884,7 @@ def e2e_measure(L, code, wl, args, dev, frame0, count, k, world):
     # the rank's frames, generated once on the device and parked in host memory (untimed)
     seed = wl.frame_seeds[0]
     for c in range(nchunks):
-        a, m = c * Fc, min(Fc, F - c * Fc)
+        a, m = sizes[c]
         b = bufs[0]
         L.ldpc_gen_info(seed, frame0 + a, m, k, b["info"])
         L.ldpc_encode(code, b["info"], b["cw"], m)
@@ -877,7 +892,8 @@ def e2e_measure(L, code, wl, args, dev, frame0, count, k, world):
         h_info[a:a + m].copy_(b["info"][:m])
         h_llr[a:a + m].copy_(b["llr"][:m])
     d_ctr = torch.zeros(6, dtype=torch.int64, device=dev)
-    wsb = L.ldpc_decode_workspace_bytes(code, Fc, wl.max_iter, wl.early_term, args.variant)
+    wsb = max(L.ldpc_decode_workspace_bytes(code, m, wl.max_iter, wl.early_term, args.variant)
+              for m in sorted({m for _, m in sizes}))
     d_ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev) if wsb else None
     s_in, s_cmp, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     ev_in = [torch.cuda.Event() for _ in range(2)]
@@ -890,7 +906,7 @@ def e2e_measure(L, code, wl, args, dev, frame0, count, k, world):
         with torch.cuda.stream(s_cmp):
             d_ctr.zero_()
         for c in range(nchunks):
-            a, m, i = c * Fc, min(Fc, F - c * Fc), c % 2
+            (a, m), i = sizes[c], c % 2
             b = bufs[i]
             if c >= 2:
                 s_in.wait_event(ev_cmp[i])          # buffer i's inputs consumed
@@ -936,8 +952,8 @@ def e2e_measure(L, code, wl, args, dev, frame0, count, k, world):
     bo = F * nw * 4 + 6 * 8
     return {"value": int(frames_all[0]) * steps * k / (ms / 1e3) / 1e9, "unit": "Gbit/s", "h2d_bytes_per_step": bi,
             "d2h_bytes_per_step": bo, "frames_per_gpu_per_step": F,
-            "note": f"pinned host buffers; H2D / encode+decode+count / D2H pipelined over {nchunks} chunks of "
-                    f"{Fc} frames on three streams; max over ranks" +
+            "note": f"pinned host buffers; H2D / encode+decode+count / D2H pipelined over {nchunks} chunks (ramping "
+                    f"{sizes[0][1]} -> {Fc} frames) on three streams; max over ranks" +
                     ("" if F == count else f"; sample of {F} of the rank's {count} frames (pinned-memory cap "
                                            f"{E2E_PINNED_BYTES / 1e9:.0f} GB over all ranks)")}
 

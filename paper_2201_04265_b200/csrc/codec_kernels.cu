@@ -135,40 +135,52 @@ __global__ void __launch_bounds__(256) encode_assemble_kernel(const DeviceCode c
     }
 }
 
-// Assemble, warp per frame (n <= 65536): the inverse permutation lives in
-// shared memory as 16-bit positions, loaded once per CTA, and every warp
-// scatters whole frames with its own staging rows -- no CTA barrier per
-// frame, and pinv is not re-read from L2 for every frame (it was 4 bytes per
-// codeword bit and frame in encode_assemble_kernel).  Same output bits.
+// Assemble by deposits, warp per frame: codeword word j is the next message
+// bits deposited into its info mask OR the next parity bits deposited into
+// its parity mask (both halves of perm ascend; host_code.cpp
+// assemble_table).  Lane l builds words l, l + 32, ...: two 32-bit windows
+// of the staged message / parity rows (funnel shifts), two five-step
+// expands, one coalesced store -- instead of one ballot per 32 bits with a
+// pinv gather per bit (encode_assemble_kernel).  Same output bits.
 constexpr int kAsmWarps = 8;
-__global__ void __launch_bounds__(kAsmWarps * 32) encode_assemble_warp_kernel(const DeviceCode code,
-                                                                              const uint32_t *__restrict__ info,
-                                                                              uint32_t *__restrict__ cw,
-                                                                              int64_t frames) {
+__device__ __forceinline__ uint32_t expand32(uint32_t x, const uint32_t *mv, uint32_t m) {
+#pragma unroll
+    for (int i = 4; i >= 0; --i) {
+        const uint32_t t = x << (1 << i);
+        x = (x & ~mv[i]) | (t & mv[i]);
+    }
+    return x & m;
+}
+__global__ void __launch_bounds__(kAsmWarps * 32) encode_assemble_dep_kernel(const DeviceCode code,
+                                                                             const uint32_t *__restrict__ info,
+                                                                             uint32_t *__restrict__ cw,
+                                                                             int64_t frames) {
     extern __shared__ __align__(16) uint32_t asm_smem[];
     const int kw = code.kw, nw = code.nw, k = code.k, n = code.n;
     const int npw = (n - k + 31) / 32;
-    const int rw = kw + npw;
-    uint16_t *pinv16 = reinterpret_cast<uint16_t *>(asm_smem + size_t(kAsmWarps) * rw);
-    for (int v = threadIdx.x; v < n; v += blockDim.x) pinv16[v] = uint16_t(__ldg(code.pinv + v));
-    __syncthreads();
+    const int rw = kw + npw + 2;                 // one zero word behind each row (funnel shifts)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t *mrow = asm_smem + size_t(warp) * rw, *prow = mrow + kw;
+    uint32_t *mrow = asm_smem + size_t(warp) * rw, *prow = mrow + kw + 1;
     const int64_t gw = int64_t(blockIdx.x) * kAsmWarps + warp, nwarps = int64_t(gridDim.x) * kAsmWarps;
+    const uint4 *tab = reinterpret_cast<const uint4 *>(code.asmtab);
     for (int64_t f = gw; f < frames; f += nwarps) {
         uint32_t *row = cw + f * int64_t(nw);
         for (int i = lane; i < kw; i += 32) mrow[i] = __ldg(info + f * int64_t(kw) + i);
         for (int i = lane; i < npw; i += 32) prow[i] = row[nw - npw + i];
+        if (lane == 0) {
+            mrow[kw] = 0u;
+            prow[npw] = 0u;
+        }
         __syncwarp();
-        for (int v0 = 0; v0 < nw * 32; v0 += 32) {
-            const int v = v0 + lane;
-            uint32_t bit = 0u;
-            if (v < n) {
-                const int t = pinv16[v];
-                bit = t < k ? (mrow[t >> 5] >> (t & 31)) & 1u : (prow[(t - k) >> 5] >> ((t - k) & 31)) & 1u;
-            }
-            const uint32_t word = __ballot_sync(0xffffffffu, bit != 0u);
-            if (lane == 0) row[v0 >> 5] = word;
+        for (int j = lane; j < nw; j += 32) {
+            const uint4 h = __ldg(tab + 4 * j), u = __ldg(tab + 4 * j + 1), v = __ldg(tab + 4 * j + 2),
+                        w = __ldg(tab + 4 * j + 3);
+            const uint32_t mi = h.x, mp = h.y, a = h.z, b = 32u * uint32_t(j) - a;
+            const uint32_t mvi[5] = {u.x, u.y, u.z, u.w, v.x}, mvp[5] = {v.y, v.z, v.w, w.x, w.y};
+            uint32_t x = 0u, y = 0u;
+            if (mi) x = __funnelshift_r(mrow[a >> 5], mrow[(a >> 5) + 1], a & 31u);
+            if (mp) y = __funnelshift_r(prow[b >> 5], prow[(b >> 5) + 1], b & 31u);
+            row[j] = expand32(x, mvi, mi) | expand32(y, mvp, mp);
         }
         __syncwarp();
     }
@@ -354,16 +366,12 @@ ldpc_status ldpc_encode(const ldpc_code *code, const uint32_t *d_info, uint32_t 
         const dim3 grid(col_tiles, unsigned((nf + ldpc::kEncTF - 1) / ldpc::kEncTF));
         ldpc::encode_parity_kernel<<<grid, 256, 0, s>>>(D, d_info + f0 * D.kw, d_cw + f0 * D.nw, nf);
     }
-    const size_t smemw = sizeof(uint32_t) * size_t(ldpc::kAsmWarps) * size_t(D.kw + (D.n - D.k + 31) / 32) +
-                         sizeof(uint16_t) * size_t(D.n);
+    const size_t smemw = sizeof(uint32_t) * size_t(ldpc::kAsmWarps) * size_t(D.kw + (D.n - D.k + 31) / 32 + 2);
     const char *aenv = std::getenv("LDPC_ASM_WARP");
-    // only where >= 2 CTAs (16 warps) fit an SM: C5's 194 KB per CTA leaves 8
-    // warps per SM, measured slower than the CTA-per-frame kernel (74.7 vs
-    // 66.0 ms per 65,536 frames; C4 15.1 -> 14.1 ms per 200,000)
-    if (D.n <= 65536 && smemw <= 108 * 1024 && !(aenv && std::atoi(aenv) == 0)) {
+    if (D.asmtab && smemw <= 200 * 1024 && !(aenv && std::atoi(aenv) == 0)) {
         static size_t attr = 0;
         if (smemw > 48 * 1024 && smemw > attr) {
-            if (cudaFuncSetAttribute(ldpc::encode_assemble_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            if (cudaFuncSetAttribute(ldpc::encode_assemble_dep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(smemw)) != cudaSuccess)
                 return LDPC_ERR_CUDA;
             attr = smemw;
@@ -372,8 +380,8 @@ ldpc_status ldpc_encode(const ldpc_code *code, const uint32_t *d_info, uint32_t 
         const int per_sm = int(std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / (smemw + 1024))));
         const int grid = int(std::min<int64_t>((frames + ldpc::kAsmWarps - 1) / ldpc::kAsmWarps,
                                                int64_t(ldpc::sm_count()) * per_sm));
-        ldpc::encode_assemble_warp_kernel<<<std::max(grid, 1), ldpc::kAsmWarps * 32, smemw, s>>>(D, d_info, d_cw,
-                                                                                              frames);
+        ldpc::encode_assemble_dep_kernel<<<std::max(grid, 1), ldpc::kAsmWarps * 32, smemw, s>>>(D, d_info, d_cw,
+                                                                                             frames);
         return cudaGetLastError() == cudaSuccess ? LDPC_OK : LDPC_ERR_CUDA;
     }
     const size_t smem = sizeof(uint32_t) * size_t(D.kw + (D.n - D.k + 31) / 32);

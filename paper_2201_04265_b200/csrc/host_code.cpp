@@ -202,6 +202,7 @@ DeviceLayout compute_layout(const ldpc_code &c, bool with_G) {
         L.pinv = off;  off = align256(off + sizeof(int32_t) * size_t(c.n));
         const size_t npp = (size_t(c.n - c.k) + kEncColTile - 1) / kEncColTile * kEncColTile;
         L.pt = off;    off = align256(off + sizeof(uint32_t) * std::max<size_t>(kw * npp, 1));
+        L.asmtab = off; off = align256(off + sizeof(uint32_t) * 16 * ((size_t(c.n) + 31) / 32));
     }
     L.total = off;
     return L;
@@ -722,6 +723,56 @@ int32_t xband_tables(const ldpc_code &c, int C, std::vector<uint16_t> &ridx, std
     }
     return cap;
 }
+// Encoder assemble table (codec_kernels.cu encode_assemble_dep_kernel).  The
+// codeword in H order interleaves the message bits (positions perm[0..k)) and
+// the parity bits (perm[k..n)); both halves of perm ascend (reading Q13:
+// [free ascending, pivots ascending]), so codeword word j takes the next
+// popc(info mask) message bits starting at message bit a_j and the next
+// parity bits starting at 32 j - a_j, each deposited into its mask's
+// positions.  The deposit is Hacker's Delight's expand (7-5) with the five
+// move masks of each mask precomputed here.  Per word, 16 uint32: info mask,
+// parity mask, a_j, 0, move masks of the info mask [5], of the parity mask
+// [5], 0 x 3.  False (no table) if a half of perm does not ascend.
+static void expand_moves(uint32_t m, uint32_t mv_out[5]) {
+    uint32_t mk = ~m << 1;
+    for (int i = 0; i < 5; ++i) {
+        uint32_t mp = mk ^ (mk << 1);
+        mp ^= mp << 2;
+        mp ^= mp << 4;
+        mp ^= mp << 8;
+        mp ^= mp << 16;
+        const uint32_t mv = mp & m;
+        mv_out[i] = mv;
+        m = (m ^ mv) | (mv >> (1 << i));
+        mk &= ~mp;
+    }
+}
+bool assemble_table(const ldpc_code &c, std::vector<uint32_t> &tab) {
+    const int32_t n = c.n, k = c.k;
+    for (int32_t t = 1; t < n; ++t)
+        if (t != k && c.perm[size_t(t)] <= c.perm[size_t(t - 1)]) return false;
+    const int32_t nw = (n + 31) / 32;
+    tab.assign(size_t(nw) * 16, 0u);
+    int32_t a = 0;          // message bits before word j
+    for (int32_t j = 0; j < nw; ++j) {
+        uint32_t mi = 0, mp = 0;
+        for (int32_t b = 0; b < 32; ++b) {
+            const int32_t v = 32 * j + b;
+            if (v >= n) break;
+            if (c.pinv[size_t(v)] < k) mi |= 1u << b;
+            else mp |= 1u << b;
+        }
+        uint32_t *e = &tab[size_t(j) * 16];
+        e[0] = mi;
+        e[1] = mp;
+        e[2] = uint32_t(a);
+        expand_moves(mi, e + 4);
+        expand_moves(mp, e + 9);
+        a += __builtin_popcount(mi);
+    }
+    return a == k;
+}
+
 }  // namespace ldpc
 
 extern "C" {
@@ -1161,10 +1212,14 @@ ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, vo
                      put(L.xband_seg, seg.data(), sizeof(int32_t) * seg.size());
         }
     }
-    if (ok && code->has_G)
+    bool asm_ok = false;
+    if (ok && code->has_G) {
+        std::vector<uint32_t> tab;
+        asm_ok = ldpc::assemble_table(*code, tab);
         ok = put(L.perm, code->perm.data(), sizeof(int32_t) * code->perm.size()) &&
              put(L.pinv, code->pinv.data(), sizeof(int32_t) * code->pinv.size()) &&
-             put_pt(L.pt);
+             put_pt(L.pt) && (!asm_ok || put(L.asmtab, tab.data(), sizeof(uint32_t) * tab.size()));
+    }
     // The host vectors are pageable: cudaMemcpyAsync from pageable memory is
     // staged synchronously, so they may be reused as soon as the call returns.
     if (!ok) return LDPC_ERR_CUDA;
@@ -1203,6 +1258,7 @@ ldpc_status ldpc_code_bind_device(ldpc_code *code, void *d_buf, size_t bytes, vo
     D.xband_sidx = D.xcluster ? reinterpret_cast<const uint16_t *>(base + L.xband_sidx) : nullptr;
     D.xband_seg = D.xcluster ? reinterpret_cast<const int32_t *>(base + L.xband_seg) : nullptr;
     D.pt = code->has_G ? reinterpret_cast<const uint32_t *>(base + L.pt) : nullptr;
+    D.asmtab = (code->has_G && asm_ok) ? reinterpret_cast<const uint32_t *>(base + L.asmtab) : nullptr;
     D.npar_pad = code->has_G ? (code->n - code->k + ldpc::kEncColTile - 1) / ldpc::kEncColTile * ldpc::kEncColTile : 0;
     return LDPC_OK;
 }

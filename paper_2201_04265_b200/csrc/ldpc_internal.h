@@ -28,6 +28,8 @@ struct DeviceLayout {
     size_t perm = 0;       // int32 [n]         (after make_G)
     size_t pinv = 0;       // int32 [n]         inverse of perm: position of column v in [m | mP]
     size_t pt = 0;         // uint32 [kw][npar_pad] P by message word: bit i of [w][b] = P[32w+i][b]
+    size_t asmtab = 0;     // uint32 [nw][16] encoder assemble: per codeword word, its info/parity bit
+                           // masks, the first info bit's index and the expand masks (host_code.cpp)
     // Gallager band view (ldpc_make_H codes only), used by the band kernel:
     size_t band_lidx = 0;  // int32 [(wc-1)*n]  edge (band b>=1, position p) -> byte offset of L[pi_b[p]]
     size_t band_vpos = 0;  // int32 [n*(wc-1)]  variable v, band b>=1 -> byte offset of its E in E_hi
@@ -60,6 +62,7 @@ struct DeviceCode {
     const int32_t *perm;
     const int32_t *pinv;
     const uint32_t *pt;
+    const uint32_t *asmtab;         // null unless both halves of perm ascend (every make_G here)
     int32_t npar_pad;               // n - k rounded up to kEncColTile
     int32_t gallager, wc, wr, mb;   // band structure (mb = n / wr rows per band)
     const int32_t *band_lidx;
