@@ -148,7 +148,11 @@ const char *ldpc_status_str(ldpc_status s);
  * c[perm[t]] = m_t (t < k) and c[perm[k+b]] = XOR_a m_a P[a][b].
  * d_info: frames * ceil(k/32) uint32 (packed message bits);
  * d_cw:   frames * ceil(n/32) uint32 (packed codeword, H column order).
- * Requires make_G and bind_device after it (else LDPC_ERR_STATE). */
+ * Requires make_G and bind_device after it (else LDPC_ERR_STATE).
+ * The parity product runs on the tensor cores (exact int32 dot products of
+ * 0/1 bytes, parity = LSB) when ceil(k/32) >= 16 and the batch has at least
+ * one 256 x 256 tile per SM, else as a binary GEMM on the INT pipe; the bits
+ * are identical.  Launch errors return LDPC_ERR_CUDA. */
 ldpc_status ldpc_encode(const ldpc_code *code, const uint32_t *d_info, uint32_t *d_cw,
                         int64_t frames, void *stream);
 
@@ -203,7 +207,10 @@ ldpc_status ldpc_decode_workspace_bytes(const ldpc_code *code, int64_t frames,
  * 7 with C SMs per frame when the code has that view (lower latency: stream
  * mode, small batches), else variant 8 when there are no more frames than
  * SMs; larger frames run 7, else 5; any other H runs 8 for such batches,
- * else 1 or 2. */
+ * else 1 or 2.  Variant 7 on batches of many frame-pair rounds also runs the
+ * last frames on variant 9's groups over the SMs its 16-CTA clusters leave
+ * idle, launched as the clusters' programmatic dependent in the same call
+ * (same results; its workspace is then variant 9's). */
 ldpc_status ldpc_decode(const ldpc_code *code, const float *d_llr, int64_t frames,
                         const ldpc_decode_opts *opts, uint32_t *d_bits,
                         uint8_t *d_syndrome_ok, int32_t *d_iters, float *d_posterior,

@@ -1,6 +1,7 @@
 // codec_kernels.cu -- the encoder (Eq. 3 in standard form) and the harness
 // kernels around the decoder: info-bit generator, BPSK/AWGN channel with the
-// LLR of Eq. 4, and the error counters.  All sm_100a, no tensor cores.
+// LLR of Eq. 4, and the error counters.  All sm_100a; the tensor-core form
+// of the parity product is encode_mma.cu.
 #include <cuda_runtime.h>
 
 #include <algorithm>
