@@ -90,14 +90,14 @@ __device__ __forceinline__ bool cta_sync_or(bool p) { return __syncthreads_or(p 
 // registers), C3 (n = 3996): 2 (wr 6, 40 registers) / 3 (wr 12, 56).
 // Measured: C3-R1/2 77.6 -> 91.4% of the SFU roofline, C3-R3/4 66.9 ->
 // 69.2%, C2 51.2 -> 52.0%; C2 at 10 blocks (32 registers) 47.6%.
-constexpr int band_lb_minb(int wr, int nfix, int lpr, int wc = 0) {
+constexpr int band_lb_minb(int wr, int nfix, int lpr, int wc = 0, int b0 = 1) {
     return lpr == 2 ? BAND_LPR2_MINB
          : !BAND_NFIX_MINB ? 1
-         : nfix == 1008 ? 7 : nfix == 3996 ? (wr == 12 ? BAND_C3R34_MINB : wr == 4 ? 3 : 2)
+         : nfix == 1008 ? 7 : nfix == 3996 ? (wr == 12 ? BAND_C3R34_MINB : wr == 4 ? 3 : b0 == 2 ? 3 : 2)
          : (nfix == 1032 && wc == 3) ? BAND_T1R34_MINB : 1;
 }
 constexpr int band_lb_threads(int wr, int wc, int b0, int nfix, int lpr) {
-    return (lpr == 2 || band_lb_minb(wr, nfix, lpr, wc) > 1) ? ((nfix / wr + b0 - 1) / b0 + 31) / 32 * 32 * lpr
+    return (lpr == 2 || band_lb_minb(wr, nfix, lpr, wc, b0) > 1) ? ((nfix / wr + b0 - 1) / b0 + 31) / 32 * 32 * lpr
                                                           : (wc > 3 ? 256 : 1024);
 }
 // LPR0: lanes per band-0 row (default LPR).  C1 runs one lane per row of
@@ -105,7 +105,7 @@ constexpr int band_lb_threads(int wr, int wc, int b0, int nfix, int lpr) {
 // on 32 lanes instead of 16), halving the variable phase's chain.
 template <int WR, int WC, int B0, bool ET, int MODE, int NFIX = 0, bool GEN = false, int RPRE = 0, bool NOVOTE = false,
           int LPR = 1, int LPR0 = LPR>
-__global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_lb_minb(WR, NFIX, LPR, WC))
+__global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_lb_minb(WR, NFIX, LPR, WC, B0))
     band_kernel(const BandArgs a) {
     // measured on B200: +1.1 points on C4 (MODE 2), +0.8..1.3 on wr = 12 codes,
     // -2..3 on check-major wr = 4 / 6 codes (C3 R1/4, R1/2)

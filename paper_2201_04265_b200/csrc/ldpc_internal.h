@@ -242,6 +242,7 @@ struct BandPlan {
     bool vm = false;            // E of bands >= 1 stored variable-major
     int mode = 0;               // kernel MODE: 0 check-major, 1 VM, 2 VM + 16-bit offsets
     int lpr = 1;                // lanes per check row (2: lane-pair kernel, small batches)
+    int b0 = 1;                 // band-0 rows per thread (threads = row stride)
     size_t ws_bytes = 0;
 };
 // false when the code is not eligible (not from ldpc_make_H, unsupported

@@ -370,6 +370,7 @@ bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPla
     int b0 = std::max(1, (mb + 1023) / 1024);
     if (!std::getenv("LDPC_NO_NFIX") && band_fixed_b0(c.n, c.wr, c.wc) > b0) b0 = band_fixed_b0(c.n, c.wr, c.wc);
     if (b0 > 4) return false;
+    p.b0 = b0;
     const size_t base = size_t(c.wc) * size_t(c.n) * 4;          // E_hi + L
     const size_t with_r = base + size_t(c.n) * 4;
     const size_t reserve = 1024;                                  // static smem + driver

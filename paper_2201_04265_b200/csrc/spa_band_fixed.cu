@@ -51,7 +51,15 @@ void *lpr2(bool et, bool novote) {
 // default (0: the default).  C3-R1/4 (999 rows per band): two rows per thread,
 // 512 threads, three CTAs per SM (its launch bounds) -- one 1024-thread CTA
 // held 64 registers per thread and left two thirds of shared memory idle.
-int band_fixed_b0(int n, int wr, int wc) { return (n == 3996 && wr == 4 && wc == 3) ? 2 : 0; }
+int band_fixed_b0(int n, int wr, int wc) {
+    if (n == 3996 && wr == 4 && wc == 3) return 2;
+    // C3-R1/2: two rows per thread (352 threads, 56 registers) at three CTAs
+    // per SM instead of one row per thread (672 threads, 40 registers) at two:
+    // 4.47 -> 5.20 Gbit/s, issue 0.61 -> 0.71 (LDPC_C3R12_B0=1: the old plan)
+    const char *e = std::getenv("LDPC_C3R12_B0");
+    if (n == 3996 && wr == 6 && wc == 3 && !(e && std::atoi(e) == 1)) return 2;
+    return 0;
+}
 // Compile-time-n codes whose auto plan is variable-major E with 16-bit
 // offsets (MODE 2) although R fits shared memory: C3 (n = 3996).  Check-major
 // E left the variable phase gathering E at random banks (40% of its shared
@@ -97,6 +105,7 @@ void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode, i
     if (wc == 3 && n == 3996 && mode == 2) {      // C3, variable-major E + 16-bit offsets
         if (wr == 4 && b0 == 2) return et_pair<4, 3, 2, 2, 3996>(et);
         if (wr == 6 && b0 == 1) return et_pair<6, 3, 1, 2, 3996>(et);
+        if (wr == 6 && b0 == 2) return et_pair<6, 3, 2, 2, 3996>(et);
         if (wr == 12 && b0 == 1) return et_pair<12, 3, 1, 2, 3996>(et);
     }
     if (wc == 3 && n == 3996 && b0 == 1 && mode == 0) {

@@ -58,7 +58,9 @@ extern "C" ldpc_status ldpc_decode_simulate(const ldpc_code *code, uint64_t seed
     if (v != 0 && v != 3 && v != 4 && v != 6) return LDPC_ERR_UNSUPPORTED;
     ldpc::BandPlan bp;
     if (!ldpc::band_plan(*code, frames, opts->early_term != 0, v, bp, opts->max_iter, false)) return LDPC_ERR_UNSUPPORTED;
-    const int b0 = std::max(1, (code->n / code->wr + 1023) / 1024);
+    // the rows per thread of the band plan ldpc_decode runs (its row stride is
+    // bp.threads), so the fused kernel decodes every row, with the same warps
+    const int b0 = bp.b0;
     void *k = ldpc::pick_gen_kernel(code->n, code->wr, code->wc, b0, opts->early_term != 0, bp.mode, opts->max_iter);
     if (!k) return LDPC_ERR_UNSUPPORTED;
     if (!ldpc::ensure_smem_attribute(k, bp.smem)) return LDPC_ERR_CUDA;
