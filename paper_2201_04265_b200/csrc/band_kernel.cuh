@@ -81,6 +81,9 @@ __device__ __forceinline__ bool cta_sync_or(bool p) { return __syncthreads_or(p 
 #ifndef BAND_T1R34_MINB
 #define BAND_T1R34_MINB 8      // Table I R3/4 (96 threads): 80 registers, no spill
 #endif
+#ifndef BAND_C2B2_MINB
+#define BAND_C2B2_MINB 12      // C2 with two rows per thread (96 threads): 12 blocks (56 registers; 14 fit shared memory but spill at 40)
+#endif
 #ifndef BAND_NFIX_MINB
 #define BAND_NFIX_MINB 1
 #endif
@@ -93,7 +96,7 @@ __device__ __forceinline__ bool cta_sync_or(bool p) { return __syncthreads_or(p 
 constexpr int band_lb_minb(int wr, int nfix, int lpr, int wc = 0, int b0 = 1) {
     return lpr == 2 ? BAND_LPR2_MINB
          : !BAND_NFIX_MINB ? 1
-         : nfix == 1008 ? 7 : nfix == 3996 ? (wr == 12 ? BAND_C3R34_MINB : wr == 4 ? 3 : b0 == 2 ? 3 : 2)
+         : nfix == 1008 ? (b0 == 2 ? BAND_C2B2_MINB : 7) : nfix == 3996 ? (wr == 12 ? BAND_C3R34_MINB : wr == 4 ? 3 : b0 == 2 ? 3 : 2)
          : (nfix == 1032 && wc == 3) ? BAND_T1R34_MINB : 1;
 }
 constexpr int band_lb_threads(int wr, int wc, int b0, int nfix, int lpr) {

@@ -58,6 +58,12 @@ int band_fixed_b0(int n, int wr, int wc) {
     // 4.47 -> 5.20 Gbit/s, issue 0.61 -> 0.71 (LDPC_C3R12_B0=1: the old plan)
     const char *e = std::getenv("LDPC_C3R12_B0");
     if (n == 3996 && wr == 6 && wc == 3 && !(e && std::atoi(e) == 1)) return 2;
+    // C2: two rows per thread (96 threads, 56 registers) at 12 CTAs per SM
+    // instead of one (192 threads, 40 registers) at 7: sweep 5.13 -> 5.42
+    // Gbit/s, 1.0 dB +8% (14 CTAs at 40 registers spill: 5.09).
+    // LDPC_C2_B0=1: the old plan
+    const char *e2 = std::getenv("LDPC_C2_B0");
+    if (n == 1008 && wr == 6 && wc == 3 && !(e2 && std::atoi(e2) == 1)) return 2;
     return 0;
 }
 // Compile-time-n codes whose auto plan is variable-major E with 16-bit
@@ -95,6 +101,7 @@ void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode, i
         return et_pair<6, 3, 3, 2, 16200>(et);
     }
     if (wc == 3 && wr == 6 && n == 1008 && b0 == 1 && mode == 0) return et_pair<6, 3, 1, 0, 1008>(et);
+    if (wc == 3 && wr == 6 && n == 1008 && b0 == 2 && mode == 0) return et_pair<6, 3, 2, 0, 1008>(et);
     if (wc == 3 && wr == 6 && n == 96 && b0 == 1 && mode == 0) {     // C1: band-0 rows on lane pairs
         if (std::getenv("LDPC_NO_B0PAIR")) return et_pair_nv<6, 3, 1, 0, 96>(et, novote);
         if (et) return reinterpret_cast<void *>(&band_kernel<6, 3, 1, true, 0, 96, false, 0, false, 1, 2>);
