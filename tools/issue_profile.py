@@ -63,12 +63,22 @@ def run(cfg, frames, extra):
 
 def main():
     out_path = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "profiles", "issue.json")
-    res = {"_source": "tools/issue_profile.py: ncu --metrics " + ",".join(METRICS) +
+    # optional second argument: a comma list of workloads to re-measure, merged
+    # into the existing file (the others keep their entries)
+    only = set(sys.argv[2].split(",")) if len(sys.argv) > 2 else None
+    prev = {}
+    if only and os.path.exists(out_path):
+        with open(out_path) as f:
+            prev = json.load(f)
+    res = dict(prev)
+    res |= {"_source": "tools/issue_profile.py: ncu --metrics " + ",".join(METRICS) +
                       " over one decode launch of bench.py's launch configuration per workload; "
                       "thread_instructions_per_edge_update = 32 x warp instructions / edge-updates "
                       "(issue slots, full warps); active_lane_instructions_per_edge_update = thread "
                       "instructions (active lanes) / edge-updates"}
     for cfg, frames, extra in RUNS:
+        if only and cfg not in only:
+            continue
         line, vals, kname, rc, err = run(cfg, frames, extra)
         if not line or "smsp__inst_executed.sum" not in vals:
             print(f"{cfg}: failed rc={rc} {err}", flush=True)
