@@ -894,34 +894,40 @@ def e2e_measure(L, code, wl, args, dev, frame0, count, k, world):
     d_ctr = torch.zeros(6, dtype=torch.int64, device=dev)
     wsb = max(L.ldpc_decode_workspace_bytes(code, m, wl.max_iter, wl.early_term, args.variant)
               for m in sorted({m for _, m in sizes}))
-    d_ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev) if wsb else None
-    s_in, s_cmp, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    # one workspace and one compute stream per buffer: consecutive chunks
+    # compute on different streams, so a chunk's decode starts on the SMs the
+    # previous chunk's last frames leave idle instead of after them
+    d_ws = [torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev) if wsb else None for _ in range(2)]
+    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    s_cmp = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
     ev_in = [torch.cuda.Event() for _ in range(2)]
     ev_cmp = [torch.cuda.Event() for _ in range(2)]
     ev_out = [torch.cuda.Event() for _ in range(2)]
 
     def step():
         """Three-stage pipeline over chunks: H2D (s_in) -> encode, decode,
-        count (s_cmp) -> D2H of the decoded bits (s_out), double-buffered."""
-        with torch.cuda.stream(s_cmp):
+        count (s_cmp[c % 2]) -> D2H of the decoded bits (s_out), double-buffered."""
+        s_cmp[0].wait_stream(s_out)                 # the previous step's counters have been read
+        with torch.cuda.stream(s_cmp[0]):
             d_ctr.zero_()
+        s_cmp[1].wait_stream(s_cmp[0])
         for c in range(nchunks):
             (a, m), i = sizes[c], c % 2
-            b = bufs[i]
+            b, sc = bufs[i], s_cmp[i]
             if c >= 2:
                 s_in.wait_event(ev_cmp[i])          # buffer i's inputs consumed
             with torch.cuda.stream(s_in):
                 b["info"][:m].copy_(h_info[a:a + m], non_blocking=True)
                 b["llr"][:m].copy_(h_llr[a:a + m], non_blocking=True)
                 ev_in[i].record(s_in)
-            s_cmp.wait_event(ev_in[i])
+            sc.wait_event(ev_in[i])
             if c >= 2:
-                s_cmp.wait_event(ev_out[i])         # buffer i's bits drained
-            L.ldpc_encode(code, b["info"], b["cw"], m, stream=s_cmp)
-            L.ldpc_decode(code, b["llr"], m, b["bits"], b["syn"], b["it"], None, d_ws, wl.max_iter,
-                          wl.early_term, args.variant, stream=s_cmp)
-            L.ldpc_count_errors(code, b["info"], b["bits"], b["cw"], b["syn"], b["it"], m, d_ctr, stream=s_cmp)
-            ev_cmp[i].record(s_cmp)
+                sc.wait_event(ev_out[i])            # buffer i's bits drained
+            L.ldpc_encode(code, b["info"], b["cw"], m, stream=sc)
+            L.ldpc_decode(code, b["llr"], m, b["bits"], b["syn"], b["it"], None, d_ws[i], wl.max_iter,
+                          wl.early_term, args.variant, stream=sc)
+            L.ldpc_count_errors(code, b["info"], b["bits"], b["cw"], b["syn"], b["it"], m, d_ctr, stream=sc)
+            ev_cmp[i].record(sc)
             s_out.wait_event(ev_cmp[i])
             with torch.cuda.stream(s_out):
                 h_bits[a:a + m].copy_(b["bits"][:m], non_blocking=True)
@@ -929,7 +935,8 @@ def e2e_measure(L, code, wl, args, dev, frame0, count, k, world):
         with torch.cuda.stream(s_out):
             h_ctr.copy_(d_ctr, non_blocking=True)
 
-    s_cmp.wait_stream(torch.cuda.current_stream())
+    for sc in s_cmp:
+        sc.wait_stream(torch.cuda.current_stream())
     step()
     torch.cuda.synchronize()
     steps = max(1, args.steps)
@@ -953,7 +960,8 @@ def e2e_measure(L, code, wl, args, dev, frame0, count, k, world):
     return {"value": int(frames_all[0]) * steps * k / (ms / 1e3) / 1e9, "unit": "Gbit/s", "h2d_bytes_per_step": bi,
             "d2h_bytes_per_step": bo, "frames_per_gpu_per_step": F,
             "note": f"pinned host buffers; H2D / encode+decode+count / D2H pipelined over {nchunks} chunks (ramping "
-                    f"{sizes[0][1]} -> {Fc} frames) on three streams; max over ranks" +
+                    f"{sizes[0][1]} -> {Fc} frames) on four streams (two compute streams alternating by chunk); "
+                    f"max over ranks" +
                     ("" if F == count else f"; sample of {F} of the rank's {count} frames (pinned-memory cap "
                                            f"{E2E_PINNED_BYTES / 1e9:.0f} GB over all ranks)")}
 
