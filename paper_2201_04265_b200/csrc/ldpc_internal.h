@@ -254,7 +254,7 @@ bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPla
 // band_kernel instantiation with n compiled in (spa_band_fixed.cu), or nullptr.
 // lpr: lanes per check row (1, or 2 for the lane-pair instantiations).
 void *pick_band_kernel_fixed(int n, int wr, int wc, int b0, bool et, int mode, int max_iter, int lpr = 1);
-int band_fixed_b0(int n, int wr, int wc);
+int band_fixed_b0(int n, int wr, int wc, int64_t frames, int sms);
 bool band_fixed_vm(int n, int wr, int wc);
 // Whether the band decoder runs without psi regime votes for this code and
 // iteration count (few-iteration configs with a compile-time-n kernel).

@@ -368,7 +368,8 @@ bool band_plan(const ldpc_code &c, int64_t frames, bool et, int variant, BandPla
     const int optin = device_attribute(cudaDevAttrMaxSharedMemoryPerBlockOptin);
     if (sms < 1 || optin < 1) return false;
     int b0 = std::max(1, (mb + 1023) / 1024);
-    if (!std::getenv("LDPC_NO_NFIX") && band_fixed_b0(c.n, c.wr, c.wc) > b0) b0 = band_fixed_b0(c.n, c.wr, c.wc);
+    const int fb0 = band_fixed_b0(c.n, c.wr, c.wc, frames, sms);
+    if (!std::getenv("LDPC_NO_NFIX") && fb0 > b0) b0 = fb0;
     if (b0 > 4) return false;
     p.b0 = b0;
     const size_t base = size_t(c.wc) * size_t(c.n) * 4;          // E_hi + L

@@ -51,7 +51,7 @@ void *lpr2(bool et, bool novote) {
 // default (0: the default).  C3-R1/4 (999 rows per band): two rows per thread,
 // 512 threads, three CTAs per SM (its launch bounds) -- one 1024-thread CTA
 // held 64 registers per thread and left two thirds of shared memory idle.
-int band_fixed_b0(int n, int wr, int wc) {
+int band_fixed_b0(int n, int wr, int wc, int64_t frames, int sms) {
     if (n == 3996 && wr == 4 && wc == 3) return 2;
     // C3-R1/2: two rows per thread (352 threads, 56 registers) at three CTAs
     // per SM instead of one row per thread (672 threads, 40 registers) at two:
@@ -63,7 +63,9 @@ int band_fixed_b0(int n, int wr, int wc) {
     // Gbit/s, 1.0 dB +8% (14 CTAs at 40 registers spill: 5.09).
     // LDPC_C2_B0=1: the old plan
     const char *e2 = std::getenv("LDPC_C2_B0");
-    if (n == 1008 && wr == 6 && wc == 3 && !(e2 && std::atoi(e2) == 1)) return 2;
+    // (batches only: a lone frame -- stream mode -- keeps one row per thread,
+    // twice the warps on its SM: 100 -> 80 us per C2 frame)
+    if (n == 1008 && wr == 6 && wc == 3 && frames > sms && !(e2 && std::atoi(e2) == 1)) return 2;
     return 0;
 }
 // Compile-time-n codes whose auto plan is variable-major E with 16-bit
