@@ -57,7 +57,7 @@ int band_fixed_b0(int n, int wr, int wc, int64_t frames, int sms) {
     // per SM instead of one row per thread (672 threads, 40 registers) at two:
     // 4.47 -> 5.20 Gbit/s, issue 0.61 -> 0.71 (LDPC_C3R12_B0=1: the old plan)
     const char *e = std::getenv("LDPC_C3R12_B0");
-    if (n == 3996 && wr == 6 && wc == 3 && !(e && std::atoi(e) == 1)) return 2;
+    if (n == 3996 && wr == 6 && wc == 3 && frames > sms && !(e && std::atoi(e) == 1)) return 2;
     // C2: two rows per thread (96 threads, 56 registers) at 12 CTAs per SM
     // instead of one (192 threads, 40 registers) at 7: sweep 5.13 -> 5.42
     // Gbit/s, 1.0 dB +8% (14 CTAs at 40 registers spill: 5.09).
