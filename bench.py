@@ -738,7 +738,7 @@ def main():
 
     # ---- end to end through the public API with host buffers (rank-local)
     e2e = None if args.no_e2e else e2e_measure(L, code, wl, args, dev, main_res["frame0"], main_res["count"], k,
-                                               world)
+                                               world, expect=main_res["counters"])
 
     # ---- CPU baseline (rank 0, N = 1 only)
     cpu = None
@@ -835,7 +835,7 @@ def point_summary(wl, p, r, steps):
             "roofline_bound": r["roofline"]["bound"]}
 
 
-def e2e_measure(L, code, wl, args, dev, frame0, count, k, world):
+def e2e_measure(L, code, wl, args, dev, frame0, count, k, world, expect=None):
     """Same metric through the public API with pinned host buffers: H2D of the
     step's info bits and LLRs, encode, decode, count, D2H of the decoded bits
     and the counters, all inside the timed region.  Pinned host memory is
@@ -957,8 +957,13 @@ def e2e_measure(L, code, wl, args, dev, frame0, count, k, world):
     ms = float(t[0])
     bi = F * kw * 4 + F * n * 4
     bo = F * nw * 4 + 6 * 8
+    # the pipelined path's six counters (last step, all ranks) against the
+    # device-timed step's, when the e2e sample is the whole shard
+    c = h_ctr.to(dev)
+    LD.all_reduce_counters(c)
+    match = (c.cpu().tolist() == [int(x) for x in expect]) if (expect is not None and F == count) else None
     return {"value": int(frames_all[0]) * steps * k / (ms / 1e3) / 1e9, "unit": "Gbit/s", "h2d_bytes_per_step": bi,
-            "d2h_bytes_per_step": bo, "frames_per_gpu_per_step": F,
+            "d2h_bytes_per_step": bo, "frames_per_gpu_per_step": F, "counters_match_device": match,
             "note": f"pinned host buffers; H2D / encode+decode+count / D2H pipelined over {nchunks} chunks (ramping "
                     f"{sizes[0][1]} -> {Fc} frames) on four streams (two compute streams alternating by chunk); "
                     f"max over ranks" +
