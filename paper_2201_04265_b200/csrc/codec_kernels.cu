@@ -370,13 +370,9 @@ ldpc_status ldpc_encode(const ldpc_code *code, const uint32_t *d_info, uint32_t 
     const size_t smemw = sizeof(uint32_t) * size_t(ldpc::kAsmWarps) * size_t(D.kw + (D.n - D.k + 31) / 32 + 2);
     const char *aenv = std::getenv("LDPC_ASM_WARP");
     if (D.asmtab && smemw <= 200 * 1024 && !(aenv && std::atoi(aenv) == 0)) {
-        static size_t attr = 0;
-        if (smemw > 48 * 1024 && smemw > attr) {
-            if (cudaFuncSetAttribute(ldpc::encode_assemble_dep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(smemw)) != cudaSuccess)
-                return LDPC_ERR_CUDA;
-            attr = smemw;
-        }
+        if (smemw > 48 * 1024 &&
+            !ldpc::ensure_smem_attribute(reinterpret_cast<const void *>(&ldpc::encode_assemble_dep_kernel), smemw))
+            return LDPC_ERR_CUDA;
         // as many CTAs per SM as shared memory holds (C4: 4, i.e. 32 warps)
         const int per_sm = int(std::max<size_t>(1, std::min<size_t>(8, (220 * 1024) / (smemw + 1024))));
         const int grid = int(std::min<int64_t>((frames + ldpc::kAsmWarps - 1) / ldpc::kAsmWarps,

@@ -241,15 +241,8 @@ bool encode_parity_mma(const DeviceCode &D, const uint32_t *d_info, uint32_t *d_
     // measured 3.38 -> 3.23 Gbit/s on the MMA path)
     const int64_t tiles = (frames + kMmaTileM - 1) / kMmaTileM * ((D.npar_pad + kMmaTileN - 1) / kMmaTileN);
     if (!force && (D.kw < 16 || tiles < int64_t(device_attribute(cudaDevAttrMultiProcessorCount)))) return false;
-    static bool attr_ok = false;
-    if (!attr_ok) {
-        if (cudaFuncSetAttribute(encode_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMmaSmem)) !=
-            cudaSuccess) {
-            cudaGetLastError();
-            return false;
-        }
-        attr_ok = true;
-    }
+    // per-device, thread-safe attribute cache (host_code.cpp)
+    if (!ensure_smem_attribute(reinterpret_cast<const void *>(&encode_mma_kernel), kMmaSmem)) return false;
     const unsigned ntiles = unsigned((D.npar_pad + kMmaTileN - 1) / kMmaTileN);
     const int64_t max_chunk = int64_t(65535) * kMmaTileM;      // gridDim.y limit
     for (int64_t f0 = 0; f0 < frames; f0 += max_chunk) {
