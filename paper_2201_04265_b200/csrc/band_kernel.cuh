@@ -31,7 +31,7 @@ struct BandArgs {
     uint8_t *syn_ok;
     int32_t *iters;
     float *posterior;
-    unsigned long long *frame_counter;   // zeroed before launch
+    unsigned long long *frame_counter;   // zeroed before launch; null: frames grid-stride
     float *r_global;                     // R' per CTA slot when R does not fit in smem
     int32_t r_in_smem;
     int32_t row_stride;                  // S = ceil(mb / B0): thread t owns rows t, t+S, ...
@@ -233,8 +233,14 @@ __global__ void __launch_bounds__(band_lb_threads(WR, WC, B0, NFIX, LPR), band_l
         }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
+    // frames: claimed from the counter (dynamic, batches beyond one wave), or
+    // grid-stride when the launch holds every frame at once (no counter, so
+    // no memset node before a small batch's decode; the previous frame index
+    // stays in s_frame, so no register is live across the loop)
+    if (tt == 0) s_frame = (long long)blockIdx.x - (long long)gridDim.x;
     for (;;) {
-        if (tt == 0) s_frame = (long long)atomicAdd(a.frame_counter, 1ull);
+        if (tt == 0)
+            s_frame = a.frame_counter ? (long long)atomicAdd(a.frame_counter, 1ull) : s_frame + gridDim.x;
         if (GEN && tt < 2) s_err[tt] = 0;
         __syncthreads();
         const long long f = s_frame;

@@ -65,8 +65,11 @@ __global__ void __launch_bounds__(256) encode_parity_kernel(const DeviceCode cod
             *reinterpret_cast<uint4 *>(&ps[w][4 * c4]) = x;
         }
         __syncthreads();
+        // the last chunk's words beyond kw are zero: skip them (Table I: kw
+        // = 9..25 in one 32-word chunk)
+        const int wend = min(kEncKC, (kw - w0 + 3) & ~3);
 #pragma unroll 2
-        for (int w = 0; w < kEncKC; w += 4) {
+        for (int w = 0; w < wend; w += 4) {
             uint4 m4[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) m4[i] = *reinterpret_cast<const uint4 *>(&ms[tf * 4 + i][w]);
@@ -274,41 +277,58 @@ __global__ void channel_kernel(uint64_t seed, int64_t frame0, int64_t frames, in
 }
 
 // ---------------------------------------------------------------------------
-// Error counters: one warp per frame; block partial sums, one atomic each.
-__global__ void count_kernel(const DeviceCode code, const uint32_t *info, const uint32_t *bits, const uint32_t *cw,
-                             const uint8_t *syn, const int32_t *iters, int64_t frames,
-                             unsigned long long *counters) {
+// Error counters: a group of TPF threads per frame (a warp at
+// large batches; up to the whole 256-thread CTA when there are few frames, so
+// a small batch still spreads its bits over every SM); block partial sums,
+// one atomic each.  Each thread counts its own info-bit and codeword-bit
+// errors without a per-chunk ballot, so the loads of successive chunks are
+// independent (a cold small batch was a chain of 2 x kw/32 dependent HBM
+// loads per warp: 10 us for 1000 Table I frames); the group's sums meet in
+// shared memory before the per-frame flags (frame error, undetected) are set.
+__global__ void __launch_bounds__(256) count_kernel(const DeviceCode code, const uint32_t *info, const uint32_t *bits,
+                                                    const uint32_t *cw, const uint8_t *syn, const int32_t *iters,
+                                                    int64_t frames, int tpf, unsigned long long *counters) {
     __shared__ unsigned long long part[6];
+    __shared__ int fr_ie[8], fr_ce[8];
     if (threadIdx.x < 6) part[threadIdx.x] = 0;
-    __syncthreads();
+    const int fpb = blockDim.x / tpf;                  // frames per block pass
+    const int slot = threadIdx.x / tpf, g = threadIdx.x - slot * tpf;
     const int lane = threadIdx.x & 31;
-    const int64_t warp_global = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
     unsigned long long c0 = 0, c1 = 0, c2 = 0, c3 = 0, c4 = 0, c5 = 0;
     const int k = code.k, kw = code.kw, nw = code.nw;
-    for (int64_t f = warp_global; f < frames; f += nwarps) {
-        const uint32_t *b = bits + f * nw;
-        const uint32_t *m = info + f * kw;
-        int ie = 0;
-        for (int t0 = 0; t0 < kw * 32; t0 += 32) {
-            const int t = t0 + lane;
-            bool err = false;
-            if (t < k) {
+    const uint32_t tail = (code.n & 31) ? (1u << (code.n & 31)) - 1u : 0xffffffffu;
+    // uniform trip count over the block (every thread meets the barriers)
+    for (int64_t fb = int64_t(blockIdx.x) * fpb; fb < frames; fb += int64_t(gridDim.x) * fpb) {
+        const int64_t f = fb + slot;
+        int ie = 0, ce = 0;
+        if (f < frames) {
+            const uint32_t *b = bits + f * nw;
+            const uint32_t *m = info + f * kw;
+            const uint32_t *c = cw + f * nw;
+#pragma unroll 4
+            for (int t = g; t < k; t += tpf) {
                 const int v = __ldg(code.perm + t);
-                const uint32_t zb = (__ldg(b + (v >> 5)) >> (v & 31)) & 1u;
-                const uint32_t mb = (__ldg(m + (t >> 5)) >> (t & 31)) & 1u;
-                err = zb != mb;
+                ie += int(((__ldg(b + (v >> 5)) >> (v & 31)) ^ (__ldg(m + (t >> 5)) >> (t & 31))) & 1u);
             }
-            ie += __popc(__ballot_sync(0xffffffffu, err));
+#pragma unroll 4
+            for (int w = g; w < nw; w += tpf) {
+                uint32_t x = __ldg(b + w) ^ __ldg(c + w);
+                if (w == nw - 1) x &= tail;
+                ce += __popc(x);
+            }
         }
-        int ce = 0;
-        for (int w = lane; w < nw; w += 32) {
-            uint32_t x = __ldg(b + w) ^ __ldg(cw + f * nw + w);
-            if (w == nw - 1 && (code.n & 31)) x &= (1u << (code.n & 31)) - 1u;
-            ce += __popc(x);
-        }
+        ie = __reduce_add_sync(0xffffffffu, ie);
         ce = __reduce_add_sync(0xffffffffu, ce);
-        if (lane == 0) {
+        if (tpf > 32) {
+            if (g == 0) fr_ie[slot] = 0, fr_ce[slot] = 0;
+            __syncthreads();
+            if (lane == 0) atomicAdd(&fr_ie[slot], ie), atomicAdd(&fr_ce[slot], ce);
+            __syncthreads();
+            ie = fr_ie[slot];
+            ce = fr_ce[slot];
+            __syncthreads();                           // read before the next pass resets them
+        }
+        if (g == 0 && f < frames) {
             c0 += ie;
             c1 += ce;
             c2 += ie > 0;
@@ -317,7 +337,8 @@ __global__ void count_kernel(const DeviceCode code, const uint32_t *info, const 
             c5 += 1;
         }
     }
-    if (lane == 0) {
+    __syncthreads();
+    if (g == 0 && (c5 | c4)) {
         atomicAdd(&part[0], c0);
         atomicAdd(&part[1], c1);
         atomicAdd(&part[2], c2);
@@ -421,9 +442,15 @@ ldpc_status ldpc_count_errors(const ldpc_code *code, const uint32_t *d_info, con
     if (!code->has_G || !code->bound_G || !code->d_buf) return LDPC_ERR_STATE;
     if (frames == 0) return LDPC_OK;
     if (!d_info || !d_bits || !d_cw || !d_syndrome_ok || !d_iters || !d_counters6) return LDPC_ERR_ARG;
-    const int grid = int(std::min<int64_t>((frames + 7) / 8, int64_t(ldpc::sm_count()) * 8));
+    // threads per frame: a warp once the batch fills 8 warps on every SM,
+    // else up to 256 so a small batch is spread over the whole GPU
+    const int64_t sms = ldpc::sm_count();
+    int tpf = 32;
+    while (tpf < 256 && frames * int64_t(tpf) * 2 <= sms * 256 * 8) tpf *= 2;
+    const int fpb = 256 / tpf;
+    const int grid = int(std::min<int64_t>((frames + fpb - 1) / fpb, sms * 8));
     ldpc::count_kernel<<<dim3(unsigned(std::max(grid, 1))), 256, 0, static_cast<cudaStream_t>(stream)>>>(
-        code->dev, d_info, d_bits, d_cw, d_syndrome_ok, d_iters, frames,
+        code->dev, d_info, d_bits, d_cw, d_syndrome_ok, d_iters, frames, tpf,
         reinterpret_cast<unsigned long long *>(d_counters6));
     return cudaGetLastError() == cudaSuccess ? LDPC_OK : LDPC_ERR_CUDA;
 }
