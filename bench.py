@@ -72,6 +72,10 @@ def parse():
     ap.add_argument("--ebn0", type=float, default=None, help="override the config's Eb/N0 in dB (measurement variant)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the end-to-end arm (profiling runs)")
+    ap.add_argument("--no-sweep-one-launch", action="store_true",
+                    help="skip the sweep's one-launch measurement (configs with several Eb/N0 points)")
+    ap.add_argument("--sweep-order", choices=["asc", "desc"], default="asc",
+                    help="one-launch sweep: points by ascending Eb/N0 (longest-running frames first, default) or descending (A/B)")
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--eager", action="store_true", help="launch the step's kernels eagerly instead of replaying a CUDA graph")
     ap.add_argument("--mode", choices=["batch", "stream", "simulate"], default="batch",
@@ -737,6 +741,10 @@ def main():
     k = main_res["k"]
 
     # ---- end to end through the public API with host buffers (rank-local)
+    one_launch = None
+    if len(results) > 1 and not args.no_sweep_one_launch:
+        one_launch = measure_sweep_one_launch(args, L, code, wl, points, results, dev, rank, world, launched, sms,
+                                              props)
     e2e = None if args.no_e2e else e2e_measure(L, code, wl, args, dev, main_res["frame0"], main_res["count"], k,
                                                world, expect=main_res["counters"])
 
@@ -782,6 +790,8 @@ def main():
         if len(results) > 1:
             line["points"] = [point_summary(wl, p, r, args.steps) for p, r in zip(points, results)]
             line["sweep_fit"] = sweep_fit(wl, results, args.steps)
+            if one_launch is not None:
+                line["sweep_one_launch"] = one_launch
             line["config"]["ebn0_db"] = list(wl.ebn0_db)
             line["config"]["frame_seed"] = list(wl.frame_seeds)
             line["config"]["workload"] += f" (sweep {', '.join(str(x) for x in wl.ebn0_db)} dB)"
@@ -789,6 +799,137 @@ def main():
     if launched:
         dist.destroy_process_group()
     return 0
+
+
+def measure_sweep_one_launch(args, L, code, wl, points, results, dev, rank, world, launched, sms, props):
+    """The whole Eb/N0 sweep as ONE step: the points' frames (each rank's Eq. 9
+    share of every point) form one batch, ordered by ascending Eb/N0 so the
+    frames that run longest start first and the batch ends on the ones that
+    converge in a few iterations; one ldpc_encode, one ldpc_decode (early
+    termination) and one ldpc_count_errors per point slice (per-point BER/FER).
+    Frames are independent, so every frame decodes as it does in
+    its own point's launch; the per-point counters are compared with those of
+    the per-point steps.  Same timing rules as measure_point."""
+    import torch
+    import torch.distributed as dist
+
+    total = args.frames or wl.frames
+    if getattr(args, "sweep_order", "asc") == "desc":   # A/B: shortest-running frames first
+        points, results = list(points)[::-1], list(results)[::-1]
+    shares = [rank_share(total, rank, world, args.scaling) for _ in points]
+    offs = [0]
+    for _, c in shares:
+        offs.append(offs[-1] + c)
+    F = offs[-1]
+    k, n = code.info.k, code.info.n
+    kw, nw = L.words(k), L.words(n)
+    Fa = max(F, 1)
+    d_info = torch.empty((Fa, kw), dtype=torch.int32, device=dev)
+    d_cw = torch.empty((Fa, nw), dtype=torch.int32, device=dev)
+    d_llr = torch.empty((Fa, n), dtype=torch.float32, device=dev)
+    d_bits = torch.empty((Fa, nw), dtype=torch.int32, device=dev)
+    d_syn = torch.empty(Fa, dtype=torch.uint8, device=dev)
+    d_it = torch.empty(Fa, dtype=torch.int32, device=dev)
+    d_ctr = torch.zeros((len(points), 6), dtype=torch.int64, device=dev)
+    wsb = L.ldpc_decode_workspace_bytes(code, Fa, wl.max_iter, wl.early_term, args.variant)
+    d_ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=dev) if wsb else None
+    for i, p in enumerate(points):
+        f0, c = shares[i]
+        if c:
+            a = offs[i]
+            L.ldpc_gen_info(wl.frame_seeds[p], f0, c, k, d_info[a:a + c])
+            L.ldpc_encode(code, d_info[a:a + c], d_cw[a:a + c], c)
+            L.ldpc_channel(code, wl.frame_seeds[p], f0, c, d_cw[a:a + c], wl.sigma(p), d_llr[a:a + c])
+    ev = (torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
+
+    def device_work(s):
+        memset_async(d_ctr, s)
+        if F == 0:
+            return
+        L.ldpc_encode(code, d_info, d_cw, F, stream=s)
+        ev[0].record(s)
+        L.ldpc_decode(code, d_llr, F, d_bits, d_syn, d_it, None, d_ws, wl.max_iter, wl.early_term, args.variant,
+                      stream=s)
+        ev[1].record(s)
+        for i in range(len(points)):
+            a, c = offs[i], shares[i][1]
+            if c:
+                L.ldpc_count_errors(code, d_info[a:a + c], d_bits[a:a + c], d_cw[a:a + c], d_syn[a:a + c],
+                                    d_it[a:a + c], c, d_ctr[i], stream=s)
+
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    device_work(stream)
+    torch.cuda.synchronize()
+    graph, launches = None, None
+    if not args.eager:
+        graph = torch.cuda.CUDAGraph(keep_graph=True)
+        cap = torch.cuda.Stream()
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(graph, stream=cap):
+                device_work(cap)
+        torch.cuda.synchronize()
+        launches = graph_kernel_launches(graph)
+        graph.instantiate()
+
+    def step():
+        if graph is not None:
+            graph.replay()
+        else:
+            device_work(stream)
+        if launched:
+            reduce_step(d_ctr)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    l2 = int(getattr(props, "L2_cache_size", 126 * 2**20) or 126 * 2**20)
+    in_bytes = F * n * 4
+    flush = torch.empty(l2, dtype=torch.int32, device=dev) if in_bytes < 2 * l2 else None
+    if launched:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms, dec_ms = [], []
+    ctr = None
+    for _ in range(args.steps):
+        if flush is not None:
+            flush.add_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        dec_ms.append(ev[0].elapsed_time(ev[1]) if F else 0.0)
+        ctr = d_ctr.cpu().numpy().tolist()
+    if launched:
+        dist.barrier()
+    t = torch.tensor([sum(step_ms), sum(dec_ms)], dtype=torch.float64, device=dev)
+    reduce_step(None, t)
+    total_ms, dec_total_ms = float(t[0]), float(t[1])
+    frames_all = sum(c[5] for c in ctr)
+    it_all = sum(c[4] for c in ctr)
+    clock_mhz = measured_peaks().get("sm_max_mhz", 1965.0)
+    peak = sms * MUFU_PER_CLK_PER_SM * clock_mhz * 1e6 / MUFU_PER_EDGE_UPDATE / 1e9
+    it_rank = it_all / max(world, 1)           # the slowest rank's own edge-updates (equal shares up to Eq. 9's remainder)
+    ach = it_rank * wl.edges / (dec_total_ms / args.steps / 1e3) / 1e9 if dec_total_ms > 0 else 0.0
+    per_point = sum(r["total_ms"] for r in results) / args.steps
+    return {
+        "value": frames_all * k * args.steps / (total_ms / 1e3) / 1e9, "unit": "Gbit/s",
+        "ms_per_step": total_ms / args.steps, "decode_ms_per_step": dec_total_ms / args.steps,
+        "frames_per_step": frames_all, "mean_iterations": it_all / max(frames_all, 1),
+        "edge_updates_per_s": it_all * wl.edges * args.steps / (total_ms / 1e3),
+        "roofline_frac_on_executed_iterations": ach / peak,
+        "counters_match_points": [list(map(int, c)) for c in ctr] == [list(map(int, r["counters"])) for r in results],
+        "vs_points_one_by_one": per_point / (total_ms / args.steps),
+        "gpu_launches_per_step": launches,
+        "l2_policy": ("L2 flushed before every timed step" if flush is not None else "inputs larger than 2 x L2"),
+        "order_ebn0_db": [wl.ebn0_db[p] for p in points],
+        "note": f"the {len(points)} points' frames decoded as one batch in one ldpc_decode call, in `order_ebn0_db` "
+                "(ascending Eb/N0 = longest-running frames first); count per point slice; `value`/`points` above time the "
+                "points one launch each",
+    }
 
 
 def sweep_fit(wl, results, steps):

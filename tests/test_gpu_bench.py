@@ -48,3 +48,32 @@ def test_strong_split_matches_single_rank(cfg, total, chunk):
     summed = [a + b for a, b in zip(*parts)]
     assert summed == c1, (summed, c1)
     assert c1[4] == 50 * total                                                  # fixed iterations
+
+
+def test_sweep_one_launch_counters_equal_the_points():
+    """C2's five Eb/N0 points decoded as one batch in one ldpc_decode call
+    (bench.py `sweep_one_launch`) give, per point slice, exactly the counters
+    of the points decoded one launch each: frames are independent,
+    and the iteration counts (early termination) are part of the counters."""
+    import argparse
+
+    import bench
+    L = lib()
+    t = torch()
+    wl = W.ALL["C2"]
+    code = L.ldpc_make_H(wl.n, wl.wc, wl.wr, W.CODE_SEED)
+    L.ldpc_make_G_device(code)
+    L.ldpc_code_bind_device(code)
+    args = argparse.Namespace(frames=1500, scaling="strong", chunk=16384, variant=0, eager=False, warmup=1, steps=2,
+                              ebn0=None)
+    dev = t.device("cuda", t.cuda.current_device())
+    props = t.cuda.get_device_properties(dev)
+    sms = props.multi_processor_count
+    points = list(range(len(wl.ebn0_db)))
+    results = [bench.measure_point(args, L, code, wl, p, dev, 0, 1, False, sms, props) for p in points]
+    one = bench.measure_sweep_one_launch(args, L, code, wl, points, results, dev, 0, 1, False, sms, props)
+    assert one["frames_per_step"] == 1500 * len(points)
+    assert one["counters_match_points"], one
+    its = [r["counters"][4] / r["counters"][5] for r in results]
+    assert its == sorted(its, reverse=True)          # ascending Eb/N0 = longest-running frames first
+    assert one["value"] > 0 and one["decode_ms_per_step"] > 0
