@@ -17,9 +17,11 @@
  * Parity pins (tests/test_oracle_pins.py) tie every function here to something
  * other than itself: the paper's worked examples (Fig. 1, Fig. 2), brute-force
  * bitwise-MAP on cycle-free Tanner graphs, closed forms, published PRNG
- * known-answer vectors, and algebraic invariants.  Decoding of LARGE CYCLIC
- * codes has no closed form: "parity unpinned" there except through the
- * cycle-free / closed-form pins of the same routine.
+ * known-answer vectors, and algebraic invariants.  Decoding on graphs WITH
+ * cycles is pinned to the brute-force MAP of the depth-T computation tree
+ * (T <= 3) and to the ring's closed form (any T); no function here is
+ * "parity unpinned".  For the configs' large codes at T = 50 no independent
+ * value exists: the pin there is this same routine's.
  */
 #include <math.h>
 #include <stdint.h>

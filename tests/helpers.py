@@ -135,3 +135,65 @@ def is_tree(H: np.ndarray) -> bool:
 
 def q_function(x: float) -> float:
     return 0.5 * math.erfc(x / math.sqrt(2.0))
+
+
+def computation_tree(H: np.ndarray, root: int, depth: int):
+    """The computation tree of flooding SPA (Wiberg 1996; Richardson & Urbanke,
+    Modern Coding Theory §3): the Tanner graph of H unwrapped from variable
+    `root` for `depth` check hops.  A variable copy reached through check c
+    expands through its other checks only; copies `depth` check hops from the
+    root are leaves.  Returns (var_of, parent_of, children_of): var_of[i] is the
+    original variable of tree variable i (0 = the root), children_of[j] the
+    tree variables below tree check j, parent_of[j] the tree variable above
+    it."""
+    H = np.asarray(H)
+    var_of, var_depth, var_from = [root], [0], [-1]
+    parent_of, children_of = [], []
+    i = 0
+    while i < len(var_of):
+        if var_depth[i] < depth:
+            for c in np.flatnonzero(H[:, var_of[i]]):
+                if c == var_from[i]:
+                    continue
+                kids = []
+                for u in np.flatnonzero(H[c]):
+                    if u == var_of[i]:
+                        continue
+                    var_of.append(int(u))
+                    var_depth.append(var_depth[i] + 1)
+                    var_from.append(int(c))
+                    kids.append(len(var_of) - 1)
+                parent_of.append(i)
+                children_of.append(kids)
+        i += 1
+    return var_of, parent_of, children_of
+
+
+def tree_root_map_llr(var_of, parent_of, children_of, R, max_free: int = 20):
+    """Exact bitwise-MAP LLR ln(P(x_root = 1 | y) / P(x_root = 0 | y)) of the
+    tree code defined by computation_tree(), every tree variable i observed
+    through its own copy of R[var_of[i]]: brute force over ALL codewords of the
+    tree code.  A codeword is fixed by the root, and per check by all but the
+    last of its children (the last child closes the check's parity); checks
+    appear in breadth-first order, so a check's parent is set before it.
+    Returns None if the code has more than 2^max_free codewords."""
+    free = 1 + sum(max(len(k) - 1, 0) for k in children_of)
+    if free > max_free:
+        return None
+    N = 1 << free
+    idx = np.arange(N, dtype=np.int64)
+    x = np.zeros((len(var_of), N), dtype=np.int8)
+    x[0] = idx & 1
+    b = 1
+    for p, kids in zip(parent_of, children_of):
+        if not kids:                 # a degree-1 check forces its variable to 0
+            return None
+        acc = x[p].copy()
+        for k in kids[:-1]:
+            x[k] = (idx >> b) & 1
+            b += 1
+            acc ^= x[k]
+        x[kids[-1]] = acc
+    Rt = np.asarray(R, dtype=np.float64)[np.asarray(var_of)]
+    score = Rt @ x.astype(np.float64)
+    return _lse(score[x[0] == 1]) - _lse(score[x[0] == 0])

@@ -503,3 +503,70 @@ def test_count_errors_hand_example(oracle):
     z[1, code.perm[5]] ^= 1       # one parity-bit error in frame 1
     out = oracle.count_errors(code, info, z, c, np.array([0, 1], np.uint8), np.array([3, 7], np.int32))
     assert list(out) == [1, 2, 1, 1, 10, 2]
+
+
+# ---------------------------------------------------------------------------
+# SPA on graphs WITH cycles (Alg. 1): T flooding
+# iterations give, at every variable, the exact bitwise MAP of the depth-T
+# computation tree (the graph unwrapped from that variable, every copy of a
+# variable observed through its own copy of R).  The trees are enumerated by
+# brute force (tests/helpers.py), nothing of the oracle is reused.
+
+def _k4_edge_vertex_H():
+    """Variables = the 6 edges of K4, checks = its 4 vertices: variable degree
+    2, check degree 3 (odd: exercises the (-1)^d rule, reading Q3), girth 6."""
+    edges = [(a, b) for a in range(4) for b in range(a + 1, 4)]
+    H = np.zeros((4, 6), dtype=np.uint8)
+    for j, (a, b) in enumerate(edges):
+        H[a, j] = H[b, j] = 1
+    return H
+
+
+@pytest.mark.parametrize("name", ["k4", "hamming74", "fig1"])
+def test_spa_on_cyclic_graphs_equals_map_on_computation_tree(oracle, name):
+    H = {"k4": _k4_edge_vertex_H, "hamming74": hp.hamming74_H, "fig1": lambda: hp.golden_matrix("fig1_H.txt")}[name]()
+    assert not hp.is_tree(H)
+    code = oracle.Code.from_dense(H)
+    rng = np.random.default_rng(41)
+    n = H.shape[1]
+    checked = {1: 0, 2: 0, 3: 0}
+    wrapped = 0
+    for _ in range(12):
+        R = rng.normal(0.0, 1.6, n).astype(np.float32)
+        for T in (1, 2, 3):
+            L, *_ = oracle.spa_decode(code, R, max_iter=T)
+            for v in range(n):
+                var_of, par, kids = hp.computation_tree(H, v, T)
+                want = hp.tree_root_map_llr(var_of, par, kids, R, max_free=17)
+                if want is None:
+                    continue
+                assert abs(L[0, v] - want) < 1e-9, (name, T, v, L[0, v], want)
+                checked[T] += 1
+                wrapped += int(len(set(var_of)) < len(var_of))     # some variable appears more than once
+    assert checked[1] >= 12 * n and checked[2] > 0
+    assert wrapped > 0          # the trees really unwrapped a cycle (replicated variables)
+    if name == "k4":
+        assert checked[3] == 12 * n
+        # and the result is NOT the code's MAP: cycles over-count evidence
+        L, *_ = oracle.spa_decode(code, R, max_iter=3)
+        assert np.max(np.abs(L[0] - hp.map_llr(H, R))) > 1e-3
+
+
+def test_spa_ring_closed_form(oracle):
+    """A single cycle: checks x_i + x_{i+1 mod n} = 0.  Degree-2 checks pass the
+    other input through unchanged (2 atanh(tanh(x/2)) = x), so T iterations
+    give L_v = R_v + sum_{d=1..T} (R_{v+d} + R_{v-d}) with indices mod n --
+    evidence counted again on every lap, unlike the MAP sum_u R_u."""
+    n = 5
+    H = np.zeros((n, n), dtype=np.uint8)
+    for i in range(n):
+        H[i, i] = H[i, (i + 1) % n] = 1
+    code = oracle.Code.from_dense(H)
+    rng = np.random.default_rng(42)
+    for _ in range(10):
+        R = rng.normal(0.0, 0.4, n).astype(np.float32)
+        Rd = R.astype(np.float64)
+        for T in (1, 2, 3, 7, 12):
+            L, *_ = oracle.spa_decode(code, R, max_iter=T)
+            want = np.array([Rd[v] + sum(Rd[(v + d) % n] + Rd[(v - d) % n] for d in range(1, T + 1)) for v in range(n)])
+            assert np.max(np.abs(L[0] - want)) < 1e-9
