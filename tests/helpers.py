@@ -197,3 +197,58 @@ def tree_root_map_llr(var_of, parent_of, children_of, R, max_free: int = 20):
     Rt = np.asarray(R, dtype=np.float64)[np.asarray(var_of)]
     score = Rt @ x.astype(np.float64)
     return _lse(score[x[0] == 1]) - _lse(score[x[0] == 0])
+
+
+def computation_tree_map_llr(H: np.ndarray, R, depth: int, roots=None) -> np.ndarray:
+    """Root MAP LLRs of the depth-`depth` computation trees of the variables in
+    `roots` (default: all; other entries are NaN),
+    by marginalising the tree code directly in the (log-)probability domain:
+    a subtree's likelihood given its top variable's bit is the product over
+    the checks below it of the sum, over every assignment of the check's other
+    variables with the right parity (enumerated explicitly, 2^(d-1) terms), of
+    the product of those variables' subtree likelihoods.  Subtrees depend only
+    on (variable, check it hangs from, remaining depth), so they are shared
+    between roots.  No tanh rule, no sign rule, no LLR messages: it is the
+    definition of the marginal on a tree, and is itself checked against the
+    enumeration of all tree codewords (tree_root_map_llr) in the CPU tests."""
+    import functools
+    import itertools
+    Rd = np.asarray(R, dtype=np.float64)
+    if isinstance(H, tuple):                    # (n, row_ptr, col_idx): CSR of a matrix too large to hold densely
+        nvar, rp, ci = H
+        rows = [[int(u) for u in ci[rp[c]:rp[c + 1]]] for c in range(len(rp) - 1)]
+        cols = [[] for _ in range(nvar)]
+        for c, r in enumerate(rows):
+            for u in r:
+                cols[u].append(c)
+    else:
+        H = np.asarray(H)
+        nvar = H.shape[1]
+        rows = [np.flatnonzero(H[c]).tolist() for c in range(H.shape[0])]
+        cols = [np.flatnonzero(H[:, v]).tolist() for v in range(H.shape[1])]
+
+    @functools.lru_cache(maxsize=None)
+    def below_var(v, from_c, left):
+        """(log P(subtree obs | x_v = 0), ... = 1) of the copy of v hanging from check from_c."""
+        lp = [0.0, float(Rd[v])]
+        if left > 0:
+            for c in cols[v]:
+                if c != from_c:
+                    m = below_check(c, v, left)
+                    lp[0] += m[0]
+                    lp[1] += m[1]
+        return tuple(lp)
+
+    @functools.lru_cache(maxsize=None)
+    def below_check(c, v, left):
+        kids = [below_var(u, c, left - 1) for u in rows[c] if u != v]
+        terms = ([], [])
+        for bits in itertools.product((0, 1), repeat=len(kids)):
+            terms[sum(bits) & 1].append(sum(k[b] for k, b in zip(kids, bits)))
+        return (_lse(np.array(terms[0])), _lse(np.array(terms[1])))
+
+    out = np.full(nvar, np.nan)
+    for v in (range(nvar) if roots is None else roots):
+        lp = below_var(int(v), -1, depth)
+        out[v] = lp[1] - lp[0]
+    return out

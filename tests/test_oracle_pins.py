@@ -570,3 +570,55 @@ def test_spa_ring_closed_form(oracle):
             L, *_ = oracle.spa_decode(code, R, max_iter=T)
             want = np.array([Rd[v] + sum(Rd[(v + d) % n] + Rd[(v - d) % n] for d in range(1, T + 1)) for v in range(n)])
             assert np.max(np.abs(L[0] - want)) < 1e-9
+
+
+def test_tree_marginaliser_equals_codeword_enumeration():
+    """tests/helpers.py computation_tree_map_llr (the tree code marginalised
+    check by check in the probability domain) against the enumeration of ALL
+    codewords of the same computation tree: K4's edge-vertex graph,
+    Hamming(7,4), Fig. 1; T = 1..3."""
+    rng = np.random.default_rng(44)
+    for H in (_k4_edge_vertex_H(), hp.hamming74_H(), hp.golden_matrix("fig1_H.txt")):
+        for _ in range(4):
+            R = rng.normal(0.0, 1.6, H.shape[1]).astype(np.float32)
+            done = 0
+            for T in (1, 2, 3):
+                dp = hp.computation_tree_map_llr(H, R, T)
+                for v in range(H.shape[1]):
+                    want = hp.tree_root_map_llr(*hp.computation_tree(H, v, T), R, max_free=17)
+                    if want is not None:
+                        assert abs(dp[v] - want) < 1e-10
+                        done += 1
+            assert done > H.shape[1]
+
+
+@pytest.mark.parametrize("n,wc,wr,ebn0,Ts,nroots", [(96, 3, 6, 2.0, (1, 2, 3, 4, 6), None), (1008, 3, 6, 1.5, (1, 2, 3, 5), None),
+                                                     (3996, 3, 4, 2.5, (1, 2, 4), 300), (3996, 3, 6, 2.5, (1, 3), 300),
+                                                     (1032, 3, 12, 2.5, (1, 2), 12), (1032, 9, 12, 2.5, (1,), 6),
+                                                     (3996, 3, 12, 2.5, (1, 2), 10), (16200, 3, 6, 1.5, (1, 2, 3), 150),
+                                                     (64800, 3, 6, 1.2, (1, 2), 100)])
+def test_spa_on_config_codes_equals_computation_tree_map(oracle, n, wc, wr, ebn0, Ts, nroots):
+    """The configs' own Gallager codes (C1, C2, C3, Table I, C4, C5; all with
+    cycles) at the configs' noise: T flooding iterations of the oracle
+    equal the exact MAP of the depth-T computation tree within 1e-9 at every
+    (sampled) variable.  (Beyond ~6 iterations the two fp precisions drift
+    apart on these graphs -- DESIGN.md §4 rule 2 -- so the pin stops there.)"""
+    code = oracle.make_H(n, wc, wr, 1)
+    H = (code.n, code.row_ptr, code.col_idx)        # CSR: n = 64800 does not fit densely
+    rng = np.random.default_rng(45)
+    sigma = math.sqrt(1.0 / (2.0 * (1.0 - wc / wr) * 10 ** (ebn0 / 10)))
+    y = -1.0 + sigma * rng.standard_normal((2, n))
+    R = np.clip(2.0 * y / sigma ** 2, -20, 20).astype(np.float32)
+    roots = None if nroots is None else rng.choice(n, nroots, replace=False)
+    compared = 0
+    for T in Ts:
+        L, *_ = oracle.spa_decode(code, R, max_iter=T)
+        for f in range(R.shape[0]):
+            want = hp.computation_tree_map_llr(H, R[f], T, roots)
+            sel = ~np.isnan(want)
+            assert sel.sum() == (n if roots is None else nroots)
+            if np.max(np.abs(want[sel])) > 25:          # keep clear of the clamps (reading Q7)
+                continue
+            assert np.max(np.abs(L[f][sel] - want[sel])) < 1e-9, (T, f)
+            compared += 1
+    assert compared >= len(Ts)                  # at most half the (T, frame) cases may sit near the clamps
