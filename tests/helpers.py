@@ -252,3 +252,19 @@ def computation_tree_map_llr(H: np.ndarray, R, depth: int, roots=None) -> np.nda
         lp = below_var(int(v), -1, depth)
         out[v] = lp[1] - lp[0]
     return out
+
+
+def computation_tree_first_zero_syndrome(csr, R, max_T: int):
+    """Early termination from the definition (Eq. 8 hard decisions with ties to
+    1, Eq. 1 syndrome; reading Q11: stop at the first iteration whose decisions
+    satisfy every check): the smallest T <= max_T whose exact T-iteration
+    posteriors (computation_tree_map_llr, every variable) decide a codeword.
+    Returns (T, posteriors, decisions), or (None, None, None)."""
+    n, rp, ci = csr
+    for T in range(1, max_T + 1):
+        L = computation_tree_map_llr(csr, R, T)
+        z = (L >= 0).astype(np.int64)
+        syn = np.add.reduceat(z[np.asarray(ci)], np.asarray(rp[:-1])) & 1
+        if not syn.any():
+            return T, L, z.astype(np.uint8)
+    return None, None, None

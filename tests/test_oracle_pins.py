@@ -622,3 +622,26 @@ def test_spa_on_config_codes_equals_computation_tree_map(oracle, n, wc, wr, ebn0
             assert np.max(np.abs(L[f][sel] - want[sel])) < 1e-9, (T, f)
             compared += 1
     assert compared >= len(Ts)                  # at most half the (T, frame) cases may sit near the clamps
+
+
+def test_early_termination_equals_first_zero_syndrome_of_computation_tree(oracle):
+    """C2's code at 3.0 dB: the oracle's early-terminated decode stops at the
+    first T whose exact T-iteration posteriors (tree marginaliser, not the
+    oracle) decide a codeword, with those decisions and a set syndrome flag
+    (Eqs. 1, 8; reading Q11)."""
+    code = oracle.make_H(1008, 3, 6, 1)
+    csr = (code.n, code.row_ptr, code.col_idx)
+    rng = np.random.default_rng(47)
+    sigma = math.sqrt(1.0 / (2.0 * 0.5 * 10 ** 0.3))
+    y = -1.0 + sigma * rng.standard_normal((4, 1008))
+    R = np.clip(2.0 * y / sigma ** 2, -20, 20).astype(np.float32)
+    L, z, it, so = oracle.spa_decode(code, R, max_iter=50, early_term=True)
+    stops = set()
+    for f in range(4):
+        T, Lt, zt = hp.computation_tree_first_zero_syndrome(csr, R[f], 8)
+        assert T is not None and np.min(np.abs(Lt)) > 1e-3      # decisions are not near ties
+        assert int(it[f]) == T and int(so[f]) == 1
+        assert np.array_equal(z[f], zt)
+        assert np.max(np.abs(L[f] - Lt)) < 1e-5
+        stops.add(T)
+    assert len(stops) > 1       # different stopping iterations were exercised
